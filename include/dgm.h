@@ -1,0 +1,142 @@
+/* dgm.h — C ABI of the B200 DG Maxwell operator (arXiv:1104.4208).
+ *
+ * The library applies, every explicit time step, the energy-conserving DG
+ * operator for the loss-free time-domain Maxwell equations
+ *     ε ∂E/∂t = curl H,   μ ∂H/∂t = -curl E
+ * on an affine tetrahedral mesh, in the semi-discrete form
+ *     ∂t diag(Mε, Mμ) (E,H) = [[0, -C_hᵀ],[C_h, 0]] (E,H)
+ * with the symplectic-Euler / leapfrog update.
+ * Fields are expanded per element in the paper's Dubiner basis φ_ijk
+ * under the covariant map E|_T = F_T^{-T} Σ Ê_α φ_α ∘ Φ_T^{-1}
+ * (PAPER.md:354, 379-381); the element curl is applied through the sparse
+ * difference-differential recurrences, traces by
+ * exact restriction to the face Dubiner basis, and
+ * the inverse mass is the 3x3-block-diagonal flat-element form.
+ * Readings of the paper (flux signs, upwind flux, boundary conditions, orders,
+ * orientation) are listed in DESIGN.md §Readings (G1-G15).
+ *
+ * LAYOUT.  A field (E or H) is a device array double[3][n_tet][ld] (component,
+ * element, mode): the covariant reference components Ê_m of element T, mode α
+ * in graded order (total degree ascending, then i, then j).  ld = N rounded up
+ * to a multiple of 4 (N = (p+1)(p+2)(p+3)/6); modes in [N, ld) are padding: the
+ * library never writes them and never reads them into a result.
+ *
+ * MESH.  xyz [n_vert][3] physical coordinates; tet [n_tet][4] vertex ids whose
+ * order must be strictly ascending in rep[] (local vertex v̂0..v̂3 =
+ * (0,0,0),(1,0,0),(0,1,0),(0,0,1); det F may be negative).  rep [n_vert] is
+ * the periodic representative of each vertex (NULL = identity): faces with the
+ * same representative triple are glued (periodic pairs are ordinary interior
+ * faces); a face seen once is a PEC boundary (mirror state E⁺=-E⁻, H⁺=H⁻).
+ *
+ * OWNERSHIP.  dgm_create deep-copies every host array and keeps no caller
+ * pointer.  Field and output arrays are caller-owned DEVICE memory unless the
+ * function name ends in _host.  The context owns its device tables and scratch
+ * and frees them in dgm_destroy.  Work is enqueued on the caller's stream
+ * (cudaStream_t passed as void*, NULL = legacy default stream); only
+ * dgm_energy, dgm_tables and dgm_step_host synchronise.
+ *
+ * ERRORS.  Every call returns dgm_status; nothing throws across the ABI.
+ * dgm_last_error(ctx) gives a message (element/face ids for mesh errors).
+ * A context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef DGM_H
+#define DGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dgm_ctx dgm_ctx;
+
+typedef enum {
+  DGM_OK = 0,
+  DGM_EINVAL = 1,   /* null pointer, bad size or argument                     */
+  DGM_EMESH = 2,    /* non-canonical vertex order, degenerate tet, face shared by >2 tets */
+  DGM_EORDER = 3,   /* order outside 1..DGM_PMAX                               */
+  DGM_ECUDA = 4,    /* a CUDA call failed (message has cudaGetErrorString)     */
+  DGM_ENOMEM = 5    /* allocation failed                                       */
+} dgm_status;
+
+#define DGM_PMAX 10
+
+typedef enum {
+  DGM_FLUX_CENTRAL = 0, /* H* = {{H}}, E* = {{E}} */
+  DGM_FLUX_UPWIND = 1   /* Riemann flux, Z = sqrt(μ/ε)               (reading G2)       */
+} dgm_flux;
+
+typedef struct {
+  int64_t n_vert;
+  const double *xyz;    /* [n_vert][3] host                                   */
+  int64_t n_tet;
+  const int32_t *tet;   /* [n_tet][4] host, ascending by rep[]                */
+  const int32_t *rep;   /* [n_vert] host, periodic representative; NULL = id  */
+} dgm_mesh;
+
+typedef struct {
+  int32_t flux;          /* dgm_flux                                          */
+  int32_t eps_per_elem;  /* 0: eps points to one double; 1: to [n_tet]        */
+  int32_t mu_per_elem;   /* same for mu                                       */
+} dgm_opts;
+
+/* Validate the mesh, match faces, compute per-element geometry
+ * G'_T = F_TᵀF_T / det F_T, det F_T, 1/ε_T, 1/μ_T
+ * and upload them with the order-p programs.  order in 1..DGM_PMAX.
+ * eps, mu: host, one value or [n_tet] (opts); must be > 0.  opts may be NULL
+ * (central flux, scalar eps/mu).  On error *out is NULL. */
+dgm_status dgm_create(const dgm_mesh *mesh, int order, const double *eps, const double *mu,
+                      const dgm_opts *opts, dgm_ctx **out);
+
+/* N (modes per component), ld (leading dimension), n_tet. */
+dgm_status dgm_layout(const dgm_ctx *ctx, int64_t *n_modes, int64_t *ld, int64_t *n_tet);
+
+/* Volume part of the time derivatives, after the inverse mass:
+ *   dE = Mε^{-1}(curl H, e)_T ,  dH = -Mμ^{-1}(curl E, h)_T     (device arrays, overwritten).
+ * Either output may be NULL to skip it. */
+dgm_status dgm_apply_curl(dgm_ctx *ctx, const double *E, const double *H, double *dE, double *dH,
+                          void *cuda_stream);
+
+/* Face part (numerical flux, traces, lift), after the inverse mass (reading G1):
+ *   dE = Mε^{-1}(ν×(H*-H⁻), e)_∂T ,  dH = -Mμ^{-1}(ν×(E*-E⁻), h)_∂T.
+ * accumulate != 0 adds into dE/dH instead of overwriting.  NULL output skips. */
+dgm_status dgm_apply_flux(dgm_ctx *ctx, const double *E, const double *H, double *dE, double *dH,
+                          int accumulate, void *cuda_stream);
+
+/* nsteps of the symplectic-Euler map (reading G7: H staggered)
+ *   H ← H + dt Ḣ(E, H);   E ← E + dt Ė(H, E)
+ * in place on the device arrays E, H.  Upwind self-terms use the current value
+ * of the field being updated. */
+dgm_status dgm_step(dgm_ctx *ctx, double *E, double *H, double dt, int64_t nsteps, void *cuda_stream);
+
+/* Same as dgm_step on HOST arrays (layout as above): copies E,H host→device,
+ * steps, copies back device→host, synchronises.  The context keeps the device
+ * copies between calls.  Host arrays should be pinned for full copy speed. */
+dgm_status dgm_step_host(dgm_ctx *ctx, double *E_host, double *H_host, double dt, int64_t nsteps,
+                         void *cuda_stream);
+
+/* Discrete energy ½(E,MεE) + ½(H,MμH), deterministic
+ * two-pass reduction; writes one double to *out_host and synchronises. */
+dgm_status dgm_energy(dgm_ctx *ctx, const double *E, const double *H, double *out_host, void *cuda_stream);
+
+/* Host copies of the integer tables, each [n_tet][4]:
+ *   nbr (neighbour tet, -1 on PEC), nbr_face (its local face, -1 on PEC),
+ *   sign = (-1)^f sign(det F_T), bc (0 interior incl. periodic, 1 PEC).
+ * Any pointer may be NULL. */
+dgm_status dgm_tables(const dgm_ctx *ctx, int32_t *nbr, int8_t *nbr_face, int8_t *sign, int8_t *bc);
+
+/* Host-only utility (no GPU needed): validate a mesh exactly as dgm_create
+ * does and return the integer tables of dgm_tables.  Errors as dgm_create;
+ * message via dgm_last_error(NULL). */
+dgm_status dgm_match_faces_host(const dgm_mesh *mesh, int32_t *nbr, int8_t *nbr_face, int8_t *sign, int8_t *bc);
+
+/* Number of kernel launches the last dgm_step/dgm_apply_* call enqueued. */
+int64_t dgm_last_launches(const dgm_ctx *ctx);
+
+const char *dgm_last_error(const dgm_ctx *ctx);
+void dgm_destroy(dgm_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGM_H */

@@ -1,0 +1,405 @@
+// Host side of the C ABI: mesh validation, face matching, geometry, program
+// upload and the call wrappers (SURVEY.md §3 call stacks 1-4).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "dgm_internal.h"
+
+using dgm::Geo;
+using dgm::HostProg;
+using dgm::HostProgSet;
+
+#include "generated_tables.inc"
+
+static thread_local std::string g_create_err;  // message of the last failed dgm_create
+
+namespace dgm {
+
+dgm_status set_err(dgm_ctx *c, dgm_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+}  // namespace dgm
+
+namespace {
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return dgm::set_err(ctx, e_ == cudaErrorMemoryAllocation ? DGM_ENOMEM : DGM_ECUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+struct FaceRec {
+  int32_t r[3];
+  int32_t tet;
+  int8_t f;
+};
+
+// Face f of a tet is opposite local vertex f; its vertices are the other three
+// in ascending local order (= ascending representative order; reading G9).
+const int kFaceVerts[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+
+size_t prog_bytes(const HostProg &p) {
+  size_t rows = (size_t)p.npass * 32, terms = (size_t)p.nterm * 32;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(rows * 2) * 2 + al(terms * 2) + al(terms * 8) + al((p.npass + 1) * 4) + al(p.npass + 1);
+}
+
+// Copy one program into the staging buffer at *off, return its device view.
+dgm::DevProg stage_prog(const HostProg &p, std::vector<char> &buf, size_t &off, char *dev_base) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  auto put = [&](const void *src, size_t bytes) -> char * {
+    char *d = dev_base + off;
+    if (bytes) std::memcpy(buf.data() + off, src, bytes);
+    off += al(bytes);
+    return d;
+  };
+  size_t rows = (size_t)p.npass * 32, terms = (size_t)p.nterm * 32;
+  dgm::DevProg d;
+  d.npass = p.npass;
+  d.dst = (const uint16_t *)put(p.dst, rows * 2);
+  d.cnt = (const uint16_t *)put(p.cnt, rows * 2);
+  d.src = (const uint16_t *)put(p.src, terms * 2);
+  d.coef = (const double *)put(p.coef, terms * 8);
+  d.off = (const int32_t *)put(p.off, (p.npass + 1) * 4);
+  d.sync = (const uint8_t *)put(p.sync, p.npass ? p.npass : 1);
+  return d;
+}
+
+void free_ctx(dgm_ctx *c) {
+  if (!c) return;
+  cudaFree(c->d_geo);
+  cudaFree(c->d_nbr);
+  cudaFree(c->d_nbrf);
+  cudaFree(c->d_fmet);
+  cudaFree(c->d_blob);
+  cudaFree(c->d_trX);
+  cudaFree(c->d_partial);
+  cudaFree(c->d_E);
+  cudaFree(c->d_H);
+  delete c;
+}
+
+dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *eps, const double *mu,
+                       const dgm_opts *opts) {
+  if (!m || !m->xyz || !m->tet || m->n_vert <= 0 || m->n_tet <= 0 || !eps || !mu)
+    return dgm::set_err(c, DGM_EINVAL, "null mesh/eps/mu pointer or empty mesh");
+  if (order < 1 || order > DGM_PMAX)
+    return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
+  if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0};
+  if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND) return dgm::set_err(c, DGM_EINVAL, "unknown flux");
+  const int p = order;
+  const int64_t n = m->n_tet;
+  c->p = p;
+  c->N = (p + 1) * (p + 2) * (p + 3) / 6;
+  c->NF = (p + 1) * (p + 2) / 2;
+  c->LD = (c->N + 3) & ~3;
+  c->n_tet = n;
+  c->flux = o.flux;
+  auto rep = [&](int32_t v) -> int64_t { return m->rep ? (int64_t)m->rep[v] : (int64_t)v; };
+
+  // ---- validate vertex ids and canonical (ascending-rep) order
+  for (int64_t t = 0; t < n; ++t) {
+    for (int k = 0; k < 4; ++k) {
+      int32_t v = m->tet[4 * t + k];
+      if (v < 0 || v >= m->n_vert)
+        return dgm::set_err(c, DGM_EMESH, "tet " + std::to_string(t) + ": vertex id out of range");
+    }
+    for (int k = 0; k < 3; ++k)
+      if (!(rep(m->tet[4 * t + k]) < rep(m->tet[4 * t + k + 1])))
+        return dgm::set_err(c, DGM_EMESH, "tet " + std::to_string(t) + ": vertices not strictly ascending by rep");
+  }
+  // ---- materials
+  std::vector<double> ev(n), mv(n);
+  for (int64_t t = 0; t < n; ++t) {
+    ev[t] = o.eps_per_elem ? eps[t] : eps[0];
+    mv[t] = o.mu_per_elem ? mu[t] : mu[0];
+    if (!(ev[t] > 0) || !(mv[t] > 0) || !std::isfinite(ev[t]) || !std::isfinite(mv[t]))
+      return dgm::set_err(c, DGM_EINVAL, "tet " + std::to_string(t) + ": eps/mu must be positive");
+  }
+  // ---- geometry: F = [X1-X0, X2-X0, X3-X0]
+  std::vector<Geo> geo(n);
+  std::vector<double> fmet(o.flux == DGM_FLUX_UPWIND ? n * 12 : 0);
+  std::vector<int8_t> sgn(n);
+  for (int64_t t = 0; t < n; ++t) {
+    double X[4][3];
+    for (int k = 0; k < 4; ++k)
+      for (int i = 0; i < 3; ++i) X[k][i] = m->xyz[3 * (int64_t)m->tet[4 * t + k] + i];
+    double F[3][3];
+    double L = 0;
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) F[i][j] = X[j + 1][i] - X[0][i];
+    for (int a = 0; a < 4; ++a)
+      for (int b = a + 1; b < 4; ++b) {
+        double d2 = 0;
+        for (int i = 0; i < 3; ++i) d2 += (X[a][i] - X[b][i]) * (X[a][i] - X[b][i]);
+        L = std::max(L, std::sqrt(d2));
+      }
+    double det = F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) - F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+                 F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+    if (!(std::fabs(det) > 1e-12 * L * L * L))
+      return dgm::set_err(c, DGM_EMESH, "tet " + std::to_string(t) + ": degenerate (|det F| too small)");
+    double FtF[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double s = 0;
+        for (int i = 0; i < 3; ++i) s += F[i][a] * F[i][b];
+        FtF[a][b] = s;
+      }
+    Geo &g = geo[t];
+    g.g[0] = FtF[0][0] / det;
+    g.g[1] = FtF[0][1] / det;
+    g.g[2] = FtF[0][2] / det;
+    g.g[3] = FtF[1][1] / det;
+    g.g[4] = FtF[1][2] / det;
+    g.g[5] = FtF[2][2] / det;
+    g.detF = det;
+    g.inv_eps = 1.0 / ev[t];
+    g.inv_mu = 1.0 / mv[t];
+    g.Z = std::sqrt(mv[t] / ev[t]);
+    sgn[t] = det > 0 ? 1 : -1;
+    if (o.flux == DGM_FLUX_UPWIND) {
+      for (int f = 0; f < 4; ++f) {
+        const int *fv = kFaceVerts[f];
+        double t1[3], t2[3];
+        for (int i = 0; i < 3; ++i) {
+          t1[i] = X[fv[1]][i] - X[fv[0]][i];
+          t2[i] = X[fv[2]][i] - X[fv[0]][i];
+        }
+        double g11 = t1[0] * t1[0] + t1[1] * t1[1] + t1[2] * t1[2];
+        double g12 = t1[0] * t2[0] + t1[1] * t2[1] + t1[2] * t2[2];
+        double g22 = t2[0] * t2[0] + t2[1] * t2[1] + t2[2] * t2[2];
+        double cx = t1[1] * t2[2] - t1[2] * t2[1], cy = t1[2] * t2[0] - t1[0] * t2[2], cz = t1[0] * t2[1] - t1[1] * t2[0];
+        double area = std::sqrt(cx * cx + cy * cy + cz * cz);
+        // M = |t1×t2| g^{-1},  det g = |t1×t2|²  (upwind tangential mass, reading G2)
+        fmet[12 * t + 3 * f + 0] = g22 / area;
+        fmet[12 * t + 3 * f + 1] = -g12 / area;
+        fmet[12 * t + 3 * f + 2] = g11 / area;
+      }
+    }
+  }
+  // ---- face matching: sort representative triples (deterministic)
+  std::vector<FaceRec> faces;
+  try {
+    faces.resize((size_t)n * 4);
+  } catch (const std::bad_alloc &) {
+    return dgm::set_err(c, DGM_ENOMEM, "host allocation for faces");
+  }
+  for (int64_t t = 0; t < n; ++t)
+    for (int f = 0; f < 4; ++f) {
+      FaceRec &r = faces[4 * t + f];
+      for (int k = 0; k < 3; ++k) r.r[k] = (int32_t)rep(m->tet[4 * t + kFaceVerts[f][k]]);
+      r.tet = (int32_t)t;
+      r.f = (int8_t)f;
+    }
+  std::sort(faces.begin(), faces.end(), [](const FaceRec &a, const FaceRec &b) {
+    if (a.r[0] != b.r[0]) return a.r[0] < b.r[0];
+    if (a.r[1] != b.r[1]) return a.r[1] < b.r[1];
+    if (a.r[2] != b.r[2]) return a.r[2] < b.r[2];
+    if (a.tet != b.tet) return a.tet < b.tet;
+    return a.f < b.f;
+  });
+  c->nbr.assign(n * 4, -1);
+  c->nbrf.assign(n * 4, -1);
+  c->bc.assign(n * 4, 1);
+  c->sign.assign(n * 4, 0);
+  for (size_t i = 0; i < faces.size();) {
+    size_t j = i + 1;
+    while (j < faces.size() && faces[j].r[0] == faces[i].r[0] && faces[j].r[1] == faces[i].r[1] &&
+           faces[j].r[2] == faces[i].r[2])
+      ++j;
+    if (j - i > 2)
+      return dgm::set_err(c, DGM_EMESH, "face of tet " + std::to_string(faces[i].tet) + " shared by more than two tets");
+    if (j - i == 2) {
+      const FaceRec &a = faces[i], &b = faces[i + 1];
+      c->nbr[4 * a.tet + a.f] = b.tet;
+      c->nbrf[4 * a.tet + a.f] = b.f;
+      c->nbr[4 * b.tet + b.f] = a.tet;
+      c->nbrf[4 * b.tet + b.f] = a.f;
+      c->bc[4 * a.tet + a.f] = 0;
+      c->bc[4 * b.tet + b.f] = 0;
+    }
+    i = j;
+  }
+  for (int64_t t = 0; t < n; ++t)
+    for (int f = 0; f < 4; ++f) c->sign[4 * t + f] = (int8_t)((f % 2 == 0 ? 1 : -1) * sgn[t]);
+
+  c->h_geo.swap(geo);
+  c->h_fmet.swap(fmet);
+  return DGM_OK;
+}
+
+dgm_status upload_impl(dgm_ctx *c) {
+  const int64_t n = c->n_tet;
+  const int p = c->p;
+  int dev = 0;
+  CUDA_TRY(c, cudaGetDevice(&dev));
+  CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(c, cudaMalloc(&c->d_geo, sizeof(Geo) * n));
+  CUDA_TRY(c, cudaMemcpy(c->d_geo, c->h_geo.data(), sizeof(Geo) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMalloc(&c->d_nbr, 4 * sizeof(int32_t) * n));
+  CUDA_TRY(c, cudaMemcpy(c->d_nbr, c->nbr.data(), 4 * sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMalloc(&c->d_nbrf, 4 * n));
+  CUDA_TRY(c, cudaMemcpy(c->d_nbrf, c->nbrf.data(), 4 * n, cudaMemcpyHostToDevice));
+  if (c->flux == DGM_FLUX_UPWIND) {
+    CUDA_TRY(c, cudaMalloc(&c->d_fmet, sizeof(double) * 12 * n));
+    CUDA_TRY(c, cudaMemcpy(c->d_fmet, c->h_fmet.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMalloc(&c->d_trX, sizeof(double) * n * 8 * c->NF));
+  }
+  const HostProgSet &hs = kHostProgs[p - 1];
+  size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
+  for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);
+  std::vector<char> buf(bytes, 0);
+  CUDA_TRY(c, cudaMalloc(&c->d_blob, bytes));
+  size_t off = 0;
+  char *base = (char *)c->d_blob;
+  c->progs.curl = stage_prog(hs.curl, buf, off, base);
+  for (int f = 0; f < 4; ++f) {
+    c->progs.trace[f] = stage_prog(hs.trace[f], buf, off, base);
+    c->progs.lift[f] = stage_prog(hs.lift[f], buf, off, base);
+  }
+  std::memcpy(buf.data() + off, hs.norms, c->N * 8);
+  c->progs.norms = (const double *)(base + off);
+  off += ((size_t)c->N * 8 + 255) & ~size_t(255);
+  CUDA_TRY(c, cudaMemcpy(c->d_blob, buf.data(), bytes, cudaMemcpyHostToDevice));
+  return DGM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dgm_status dgm_create(const dgm_mesh *mesh, int order, const double *eps, const double *mu, const dgm_opts *opts,
+                      dgm_ctx **out) {
+  if (!out) return DGM_EINVAL;
+  *out = nullptr;
+  dgm_ctx *c = new (std::nothrow) dgm_ctx();
+  if (!c) return DGM_ENOMEM;
+  dgm_status s = create_impl(c, mesh, order, eps, mu, opts);
+  if (s == DGM_OK) s = upload_impl(c);
+  if (s != DGM_OK) {
+    g_create_err = c->err;   // reachable as dgm_last_error(NULL)
+    free_ctx(c);
+    return s;
+  }
+  *out = c;
+  return DGM_OK;
+}
+
+dgm_status dgm_match_faces_host(const dgm_mesh *mesh, int32_t *nbr, int8_t *nbr_face, int8_t *sign, int8_t *bc) {
+  dgm_ctx tmp;
+  double one = 1.0;
+  dgm_status s = create_impl(&tmp, mesh, 1, &one, &one, nullptr);
+  if (s != DGM_OK) {
+    g_create_err = tmp.err;
+    return s;
+  }
+  return dgm_tables(&tmp, nbr, nbr_face, sign, bc);
+}
+
+dgm_status dgm_layout(const dgm_ctx *c, int64_t *n_modes, int64_t *ld, int64_t *n_tet) {
+  if (!c) return DGM_EINVAL;
+  if (n_modes) *n_modes = c->N;
+  if (ld) *ld = c->LD;
+  if (n_tet) *n_tet = c->n_tet;
+  return DGM_OK;
+}
+
+dgm_status dgm_apply_curl(dgm_ctx *c, const double *E, const double *H, double *dE, double *dH, void *stream) {
+  if (!c || !E || !H) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->launches = 0;
+  if (dE) {
+    dgm_status s = dgm::launch_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, st);
+    if (s != DGM_OK) return s;
+  }
+  if (dH) return dgm::launch_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 0, dgm::OUT_WRITE, st);
+  return DGM_OK;
+}
+
+dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *dE, double *dH, int accumulate,
+                          void *stream) {
+  if (!c || !E || !H) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  int om = accumulate ? dgm::OUT_ACCUM : dgm::OUT_WRITE;
+  c->launches = 0;
+  if (dE) {
+    if (c->flux == DGM_FLUX_UPWIND) {
+      dgm_status s = dgm::launch_traces(c, E, st);
+      if (s != DGM_OK) return s;
+    }
+    dgm_status s = dgm::launch_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, st);
+    if (s != DGM_OK) return s;
+  }
+  if (dH) {
+    if (c->flux == DGM_FLUX_UPWIND) {
+      dgm_status s = dgm::launch_traces(c, H, st);
+      if (s != DGM_OK) return s;
+    }
+    return dgm::launch_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, st);
+  }
+  return DGM_OK;
+}
+
+dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, void *stream) {
+  if (!c || !E || !H || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->launches = 0;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    dgm_status r;
+    if (c->flux == DGM_FLUX_UPWIND && (r = dgm::launch_traces(c, H, st)) != DGM_OK) return r;
+    if ((r = dgm::launch_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, st)) != DGM_OK) return r;
+    if (c->flux == DGM_FLUX_UPWIND && (r = dgm::launch_traces(c, E, st)) != DGM_OK) return r;
+    if ((r = dgm::launch_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, st)) != DGM_OK) return r;
+  }
+  return DGM_OK;
+}
+
+dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t nsteps, void *stream) {
+  if (!c || !Eh || !Hh) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t bytes = sizeof(double) * 3 * (size_t)c->n_tet * c->LD;
+  if (!c->d_E) {
+    CUDA_TRY(c, cudaMalloc(&c->d_E, bytes));
+    CUDA_TRY(c, cudaMalloc(&c->d_H, bytes));
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_E, Eh, bytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_H, Hh, bytes, cudaMemcpyHostToDevice, st));
+  dgm_status s = dgm_step(c, c->d_E, c->d_H, dt, nsteps, stream);
+  if (s != DGM_OK) return s;
+  CUDA_TRY(c, cudaMemcpyAsync(Eh, c->d_E, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaMemcpyAsync(Hh, c->d_H, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  return DGM_OK;
+}
+
+dgm_status dgm_energy(dgm_ctx *c, const double *E, const double *H, double *out, void *stream) {
+  if (!c || !E || !H || !out) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  return dgm::launch_energy(c, E, H, out, (cudaStream_t)stream);
+}
+
+dgm_status dgm_tables(const dgm_ctx *c, int32_t *nbr, int8_t *nbr_face, int8_t *sign, int8_t *bc) {
+  if (!c) return DGM_EINVAL;
+  size_t n = (size_t)c->n_tet * 4;
+  if (nbr) std::memcpy(nbr, c->nbr.data(), n * 4);
+  if (nbr_face) std::memcpy(nbr_face, c->nbrf.data(), n);
+  if (sign) std::memcpy(sign, c->sign.data(), n);
+  if (bc) std::memcpy(bc, c->bc.data(), n);
+  return DGM_OK;
+}
+
+int64_t dgm_last_launches(const dgm_ctx *c) { return c ? c->launches : 0; }
+
+const char *dgm_last_error(const dgm_ctx *c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+void dgm_destroy(dgm_ctx *c) { free_ctx(c); }
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Internal declarations shared by the host setup (dgm_host.cpp) and the
+// kernels (dgm_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/dgm.h"
+
+namespace dgm {
+
+// One level-scheduled ELL program (see gen/plan.py): pass ps covers rows
+// [ps*32, ps*32+32); its terms are stored [term][lane] from off[ps]*32.
+struct HostProg {
+  int npass, nterm;
+  const uint16_t *dst, *cnt, *src;
+  const double *coef;
+  const int32_t *off;
+  const uint8_t *sync;
+};
+struct HostProgSet {
+  int p, acc;
+  HostProg curl;
+  HostProg trace[4];
+  HostProg lift[4];
+  const double *norms;
+};
+
+struct DevProg {
+  int npass;
+  const uint16_t *__restrict__ dst;
+  const uint16_t *__restrict__ cnt;
+  const uint16_t *__restrict__ src;
+  const double *__restrict__ coef;
+  const int32_t *__restrict__ off;
+  const uint8_t *__restrict__ sync;
+};
+struct DevProgs {
+  DevProg curl;
+  DevProg trace[4];
+  DevProg lift[4];
+  const double *__restrict__ norms;
+};
+
+// Per-element geometry, 80 bytes: G' = FᵀF/det F (symmetric, 6 entries
+// g00 g01 g02 g11 g12 g22), det F, 1/ε, 1/μ, Z = sqrt(μ/ε).
+struct Geo {
+  double g[6];
+  double detF, inv_eps, inv_mu, Z;
+};
+
+enum OutMode { OUT_UPDATE = 0, OUT_WRITE = 1, OUT_ACCUM = 2 };
+enum Stage { STAGE_E = 0, STAGE_H = 1 };   // STAGE_E updates E from H (Y=H, X=E)
+
+struct StageArgs {
+  const double *Y;       // other field (curl and central-flux source)
+  double *X;             // updated field (OUT_UPDATE)
+  double *dX;            // derivative output (OUT_WRITE / OUT_ACCUM)
+  const double *trX;     // upwind: tangential traces of the updated field [n][4][2][NF]
+  const Geo *geo;
+  const int32_t *nbr;    // [n][4], -1 PEC
+  const int8_t *nbrf;    // [n][4], -1 PEC
+  const double *fmet;    // upwind: [n][4][3] M00 M01 M11
+  int64_t n_tet;
+  double dt;
+  int stage, upwind, do_curl, do_flux, out_mode;
+};
+
+}  // namespace dgm
+
+struct dgm_ctx {
+  int p = 0, N = 0, NF = 0, LD = 0;
+  int64_t n_tet = 0;
+  int flux = 0;
+  int sms = 0;
+  std::vector<int32_t> nbr;
+  std::vector<int8_t> nbrf, sign, bc;
+  std::vector<dgm::Geo> h_geo;
+  std::vector<double> h_fmet;
+  dgm::Geo *d_geo = nullptr;
+  int32_t *d_nbr = nullptr;
+  int8_t *d_nbrf = nullptr;
+  double *d_fmet = nullptr;
+  void *d_blob = nullptr;
+  dgm::DevProgs progs{};
+  double *d_trX = nullptr;     // upwind trace buffer
+  double *d_partial = nullptr; // energy partial sums
+  int64_t n_partial = 0;
+  double *d_E = nullptr, *d_H = nullptr;   // device copies for dgm_step_host
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace dgm {
+dgm_status set_err(dgm_ctx *c, dgm_status s, const std::string &msg);
+// kernels (dgm_kernels.cu)
+dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt,
+                        int do_curl, int do_flux, int out_mode, cudaStream_t st);
+dgm_status launch_traces(dgm_ctx *c, const double *X, cudaStream_t st);
+dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
+int workspace_doubles(int p);
+}  // namespace dgm

@@ -1,0 +1,461 @@
+// DG Maxwell stage kernels for sm_100a (FP64).
+//
+// One warp owns one element at a time (grid-stride over elements); the
+// element's workspace lives in shared memory.  Per element a stage does
+// (DESIGN.md "Kernels"):
+//   S1  reference curl of the source field Ŷ by the sparse recurrence sweeps
+//       (level-scheduled pull-form program from gen/plan.py)
+//   S3  tangential traces a_k = Ŷ·t̂_k on the 4 faces, own element and the
+//       neighbour's copy of each face (exact restriction)
+//   S4  numerical flux on the face modes (central or upwind, PEC mirror)
+//   S5  lift back to volume modes (traceᵀ with ‖ψ‖²/‖φ‖² folded in)
+//   S2  inverse mass + geometry: Ẋ_β = ±(1/m_T) G'_T (ĉ_β + L_β),
+//       G'_T = F_TᵀF_T/det F_T (covariant identities :367-370)
+//   S6  update X += dt Ẋ (symplectic Euler) or write Ẋ.
+#include <cstdint>
+#include <cstdio>
+
+#include "dgm_internal.h"
+
+namespace dgm {
+
+template <int P>
+struct Dim {
+  static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
+  static constexpr int NF = (P + 1) * (P + 2) / 2;
+  static constexpr int LD = (N + 3) & ~3;
+  static constexpr int ACC = 9 * N;                 // must match gen/plan.py
+  static constexpr int FLUXSZ = 8 * NF + 3 * N + 2 * NF + 3 * NF;
+  static constexpr int FLUX_BASE = (FLUXSZ <= 6 * N) ? 3 * N : 12 * N;
+  static constexpr int WS = (FLUX_BASE + FLUXSZ > 12 * N) ? FLUX_BASE + FLUXSZ : 12 * N;
+  static constexpr int WARPS_RAW = (96 * 1024) / (WS * 8);
+  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
+};
+
+// Reference face tangents t̂1 = v̂b - v̂a, t̂2 = v̂c - v̂a (reading G9).
+__constant__ double kT1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
+__constant__ double kT2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
+
+// tangential components a1, a2 of mode a on reference face F
+template <int F>
+__device__ __forceinline__ void tangential(const double *sY, int N, int a, double &a1, double &a2) {
+  if (F == 0) {
+    double y0 = sY[a];
+    a1 = sY[N + a] - y0;
+    a2 = sY[2 * N + a] - y0;
+  } else if (F == 1) {
+    a1 = sY[N + a];
+    a2 = sY[2 * N + a];
+  } else if (F == 2) {
+    a1 = sY[a];
+    a2 = sY[2 * N + a];
+  } else {
+    a1 = sY[a];
+    a2 = sY[N + a];
+  }
+}
+
+// Generic level-scheduled program: s[dst] = Σ coef * s[src]
+__device__ __forceinline__ void run_assign(const DevProg &p, double *s, int lane) {
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int row = ps * 32 + lane;
+    const unsigned d = __ldg(p.dst + row);
+    if (d != 0xFFFFu) {
+      const int c = __ldg(p.cnt + row);
+      const int o = __ldg(p.off + ps) * 32 + lane;
+      double acc = 0.0;
+      for (int t = 0; t < c; ++t) acc = fma(__ldg(p.coef + o + 32 * t), s[__ldg(p.src + o + 32 * t)], acc);
+      s[d] = acc;
+    }
+    if (__ldg(p.sync + ps)) __syncwarp();
+  }
+}
+
+// Face-F tangential traces of the volume field sY -> out[0..NF) (k=1), out[NF..2NF) (k=2)
+template <int F>
+__device__ __forceinline__ void run_trace_f(const DevProg &p, const double *sY, int N, int NF, double *out, int lane) {
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int row = ps * 32 + lane;
+    const unsigned g = __ldg(p.dst + row);
+    if (g != 0xFFFFu) {
+      const int c = __ldg(p.cnt + row);
+      const int o = __ldg(p.off + ps) * 32 + lane;
+      double t1 = 0.0, t2 = 0.0;
+      for (int t = 0; t < c; ++t) {
+        double a1, a2;
+        tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
+        const double cf = __ldg(p.coef + o + 32 * t);
+        t1 = fma(cf, a1, t1);
+        t2 = fma(cf, a2, t2);
+      }
+      out[g] = t1;
+      out[NF + g] = t2;
+    }
+  }
+}
+
+__device__ __forceinline__ void run_trace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *out,
+                                          int lane) {
+  switch (f) {
+    case 0: run_trace_f<0>(pr.trace[0], sY, N, NF, out, lane); break;
+    case 1: run_trace_f<1>(pr.trace[1], sY, N, NF, out, lane); break;
+    case 2: run_trace_f<2>(pr.trace[2], sY, N, NF, out, lane); break;
+    default: run_trace_f<3>(pr.trace[3], sY, N, NF, out, lane); break;
+  }
+}
+
+// acc[m][β] += Σ_γ L_f[β,γ] q[m][γ]
+__device__ __forceinline__ void run_lift(const DevProg &p, const double *q, int N, int NF, double *acc, int lane) {
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int row = ps * 32 + lane;
+    const unsigned b = __ldg(p.dst + row);
+    if (b != 0xFFFFu) {
+      const int c = __ldg(p.cnt + row);
+      const int o = __ldg(p.off + ps) * 32 + lane;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int t = 0; t < c; ++t) {
+        const int g = __ldg(p.src + o + 32 * t);
+        const double cf = __ldg(p.coef + o + 32 * t);
+        a0 = fma(cf, q[g], a0);
+        a1 = fma(cf, q[NF + g], a1);
+        a2 = fma(cf, q[2 * NF + g], a2);
+      }
+      acc[b] += a0;
+      acc[N + b] += a1;
+      acc[2 * N + b] += a2;
+    }
+  }
+}
+
+template <int LDv, int Nv>
+__device__ __forceinline__ void load_elem(const double *__restrict__ F, int64_t e, int64_t cstride, double *s,
+                                          int lane) {
+  for (int c = 0; c < 3; ++c) {
+    const double *src = F + c * cstride + e * LDv;
+    for (int i = lane; i < Nv; i += 32) s[c * Nv + i] = __ldg(src + i);
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(Dim<P>::WARPS * 32) stage_kernel(StageArgs a, DevProgs pr) {
+  using D = Dim<P>;
+  constexpr int N = D::N, NF = D::NF, LD = D::LD;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *s = smem + warp * D::WS;
+  double *sY = s;
+  double *sACC = s + D::ACC;
+  double *sTO = s + D::FLUX_BASE;   // own traces [4][2][NF]
+  double *sNB = sTO + 8 * NF;       // neighbour volume staging [3][N]
+  double *sTN = sNB + 3 * N;        // neighbour traces [2][NF]
+  double *sQ = sTN + 2 * NF;        // face vectors [3][NF]
+  const int64_t cstride = a.n_tet * LD;
+  const bool stageE = a.stage == STAGE_E;
+  const double mirrorY = stageE ? 1.0 : -1.0;   // PEC: H⁺=H⁻ (Y=H), E⁺=-E⁻ (Y=E)
+  const double mirrorX = stageE ? -1.0 : 1.0;
+
+  for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < a.n_tet; e += (int64_t)gridDim.x * D::WARPS) {
+    load_elem<LD, N>(a.Y, e, cstride, sY, lane);
+    __syncwarp();
+    if (a.do_curl) {
+      run_assign(pr.curl, s, lane);
+    } else {
+      for (int i = lane; i < 3 * N; i += 32) sACC[i] = 0.0;
+    }
+    __syncwarp();
+    const Geo g = a.geo[e];
+    if (a.do_flux) {
+      for (int f = 0; f < 4; ++f) run_trace(pr, f, sY, N, NF, sTO + 2 * NF * f, lane);
+      __syncwarp();
+      const double sgn = g.detF > 0 ? 1.0 : -1.0;
+      for (int f = 0; f < 4; ++f) {
+        const int nb = a.nbr[4 * e + f];
+        const int gf = a.nbrf[4 * e + f];
+        if (nb >= 0) {
+          load_elem<LD, N>(a.Y, nb, cstride, sNB, lane);
+          __syncwarp();
+          run_trace(pr, gf, sNB, N, NF, sTN, lane);
+          __syncwarp();
+        }
+        double w = 0.5, k = 0.0;
+        double Zm = g.Z, Zp = Zm;
+        if (a.upwind) {
+          if (nb >= 0) Zp = a.geo[nb].Z;
+          if (stageE) {
+            w = Zp / (Zm + Zp);
+            k = 1.0 / (Zm + Zp);
+          } else {
+            const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
+            w = Yp / (Ym + Yp);
+            k = 1.0 / (Ym + Yp);
+          }
+        }
+        const double sf = (f & 1) ? -1.0 : 1.0;
+        const double *to = sTO + 2 * NF * f;
+        for (int gm = lane; gm < NF; gm += 32) {
+          const double yo1 = to[gm], yo2 = to[NF + gm];
+          const double yn1 = nb >= 0 ? sTN[gm] : mirrorY * yo1;
+          const double yn2 = nb >= 0 ? sTN[NF + gm] : mirrorY * yo2;
+          const double d1 = w * (yn1 - yo1), d2 = w * (yn2 - yo2);
+          double q0 = sf * (d1 * kT2[f][0] - d2 * kT1[f][0]);
+          double q1 = sf * (d1 * kT2[f][1] - d2 * kT1[f][1]);
+          double q2 = sf * (d1 * kT2[f][2] - d2 * kT1[f][2]);
+          if (a.upwind) {
+            const double *tx = a.trX + ((e * 4 + f) * 2) * NF;
+            const double xo1 = tx[gm], xo2 = tx[NF + gm];
+            double xn1, xn2;
+            if (nb >= 0) {
+              const double *tn = a.trX + (((int64_t)nb * 4 + gf) * 2) * NF;
+              xn1 = tn[gm];
+              xn2 = tn[NF + gm];
+            } else {
+              xn1 = mirrorX * xo1;
+              xn2 = mirrorX * xo2;
+            }
+            const double j1 = k * (xn1 - xo1), j2 = k * (xn2 - xo2);
+            const double *M = a.fmet + 12 * e + 3 * f;
+            const double p1 = j1 * M[0] + j2 * M[1];
+            const double p2 = j1 * M[1] + j2 * M[2];
+            const double ps = (stageE ? 1.0 : -1.0) * sgn;
+            q0 += ps * (p1 * kT1[f][0] + p2 * kT2[f][0]);
+            q1 += ps * (p1 * kT1[f][1] + p2 * kT2[f][1]);
+            q2 += ps * (p1 * kT1[f][2] + p2 * kT2[f][2]);
+          }
+          sQ[gm] = q0;
+          sQ[NF + gm] = q1;
+          sQ[2 * NF + gm] = q2;
+        }
+        __syncwarp();
+        run_lift(pr.lift[f], sQ, N, NF, sACC, lane);
+        __syncwarp();
+      }
+    }
+    // S2 + S6: inverse mass with geometry, then update or write
+    const double cm = stageE ? g.inv_eps : -g.inv_mu;
+    for (int b = lane; b < N; b += 32) {
+      const double v0 = sACC[b], v1 = sACC[N + b], v2 = sACC[2 * N + b];
+      const double x0 = cm * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
+      const double x1 = cm * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
+      const double x2 = cm * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
+      const int64_t o = e * LD + b;
+      if (a.out_mode == OUT_UPDATE) {
+        a.X[o] += a.dt * x0;
+        a.X[cstride + o] += a.dt * x1;
+        a.X[2 * cstride + o] += a.dt * x2;
+      } else if (a.out_mode == OUT_WRITE) {
+        a.dX[o] = x0;
+        a.dX[cstride + o] = x1;
+        a.dX[2 * cstride + o] = x2;
+      } else {
+        a.dX[o] += x0;
+        a.dX[cstride + o] += x1;
+        a.dX[2 * cstride + o] += x2;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Upwind: tangential traces of the updated field for all elements -> trX[e][f][k][γ]
+template <int P>
+__global__ void __launch_bounds__(Dim<P>::WARPS * 32) trace_kernel(const double *__restrict__ X, double *trX,
+                                                                    int64_t n_tet, DevProgs pr) {
+  using D = Dim<P>;
+  constexpr int N = D::N, NF = D::NF, LD = D::LD;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *s = smem + warp * D::WS;
+  double *out = s + 3 * N;
+  const int64_t cstride = n_tet * LD;
+  for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < n_tet; e += (int64_t)gridDim.x * D::WARPS) {
+    load_elem<LD, N>(X, e, cstride, s, lane);
+    __syncwarp();
+    for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, out + 2 * NF * f, lane);
+    __syncwarp();
+    for (int i = lane; i < 8 * NF; i += 32) trX[e * 8 * NF + i] = out[i];
+    __syncwarp();
+  }
+}
+
+// Energy ½ Σ_T sgn(det F) Σ_α ‖φ_α‖² (ε Ê_αᵀ G'^{-1} Ê_α + μ Ĥ_αᵀ G'^{-1} Ĥ_α)
+// (|det F| F^{-1}F^{-T} = sgn G'^{-1}).  One thread
+// per element, fixed grid, per-block partials: deterministic.
+template <int P>
+__global__ void energy_kernel(const double *__restrict__ E, const double *__restrict__ H, const Geo *__restrict__ geo,
+                              const double *__restrict__ norms, int64_t n_tet, double *partial) {
+  using D = Dim<P>;
+  constexpr int N = D::N, LD = D::LD;
+  const int64_t cstride = n_tet * LD;
+  double sum = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tet; e += (int64_t)gridDim.x * blockDim.x) {
+    const Geo g = geo[e];
+    // inverse of the symmetric G'
+    const double a = g.g[0], b = g.g[1], c = g.g[2], d = g.g[3], f = g.g[4], h = g.g[5];
+    const double c00 = d * h - f * f, c01 = c * f - b * h, c02 = b * f - c * d;
+    const double c11 = a * h - c * c, c12 = b * c - a * f, c22 = a * d - b * b;
+    const double det = a * c00 + b * c01 + c * c02;
+    const double id = 1.0 / det;
+    const double eps = 1.0 / g.inv_eps, mu = 1.0 / g.inv_mu;
+    double se = 0.0, sh = 0.0;
+    for (int al = 0; al < N; ++al) {
+      const int64_t o = e * LD + al;
+      const double e0 = E[o], e1 = E[cstride + o], e2 = E[2 * cstride + o];
+      const double h0 = H[o], h1 = H[cstride + o], h2 = H[2 * cstride + o];
+      const double qe = c00 * e0 * e0 + c11 * e1 * e1 + c22 * e2 * e2 + 2.0 * (c01 * e0 * e1 + c02 * e0 * e2 + c12 * e1 * e2);
+      const double qh = c00 * h0 * h0 + c11 * h1 * h1 + c22 * h2 * h2 + 2.0 * (c01 * h0 * h1 + c02 * h0 * h2 + c12 * h1 * h2);
+      se += norms[al] * qe;
+      sh += norms[al] * qh;
+    }
+    const double sg = g.detF > 0 ? 1.0 : -1.0;
+    sum += 0.5 * sg * id * (eps * se + mu * sh);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void sum_kernel(const double *partial, int n, double *out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+// ---------------------------------------------------------------------------
+template <int P>
+static dgm_status launch_stage_p(dgm_ctx *c, const StageArgs &a, cudaStream_t st) {
+  using D = Dim<P>;
+  const size_t smem = sizeof(double) * D::WS * D::WARPS;
+  static bool attr_set = false;
+  static int occ = 0;
+  if (!attr_set) {
+    cudaFuncSetAttribute(stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<P>, D::WARPS * 32, smem);
+    if (occ < 1) occ = 1;
+    attr_set = true;
+  }
+  int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
+  int64_t grid = (int64_t)c->sms * occ;
+  if (grid > need) grid = need;
+  stage_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(a, c->progs);
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("stage_kernel: ") + cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+template <int P>
+static dgm_status launch_traces_p(dgm_ctx *c, const double *X, cudaStream_t st) {
+  using D = Dim<P>;
+  const size_t smem = sizeof(double) * D::WS * D::WARPS;
+  static bool attr_set = false;
+  static int occ = 0;
+  if (!attr_set) {
+    cudaFuncSetAttribute(trace_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace_kernel<P>, D::WARPS * 32, smem);
+    if (occ < 1) occ = 1;
+    attr_set = true;
+  }
+  int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
+  int64_t grid = (int64_t)c->sms * occ;
+  if (grid > need) grid = need;
+  trace_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(X, c->d_trX, c->n_tet, c->progs);
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("trace_kernel: ") + cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+#define DGM_DISPATCH(p, fn, ...)          \
+  switch (p) {                            \
+    case 1: return fn<1>(__VA_ARGS__);    \
+    case 2: return fn<2>(__VA_ARGS__);    \
+    case 3: return fn<3>(__VA_ARGS__);    \
+    case 4: return fn<4>(__VA_ARGS__);    \
+    case 5: return fn<5>(__VA_ARGS__);    \
+    case 6: return fn<6>(__VA_ARGS__);    \
+    case 7: return fn<7>(__VA_ARGS__);    \
+    case 8: return fn<8>(__VA_ARGS__);    \
+    case 9: return fn<9>(__VA_ARGS__);    \
+    case 10: return fn<10>(__VA_ARGS__);  \
+    default: return DGM_EORDER;           \
+  }
+
+dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
+                        int do_flux, int out_mode, cudaStream_t st) {
+  if (c->n_tet == 0) return DGM_OK;
+  StageArgs a;
+  a.Y = Y;
+  a.X = X;
+  a.dX = dX;
+  a.trX = c->d_trX;
+  a.geo = c->d_geo;
+  a.nbr = c->d_nbr;
+  a.nbrf = c->d_nbrf;
+  a.fmet = c->d_fmet;
+  a.n_tet = c->n_tet;
+  a.dt = dt;
+  a.stage = stage;
+  a.upwind = c->flux == DGM_FLUX_UPWIND && do_flux;
+  a.do_curl = do_curl;
+  a.do_flux = do_flux;
+  a.out_mode = out_mode;
+  DGM_DISPATCH(c->p, launch_stage_p, c, a, st)
+}
+
+dgm_status launch_traces(dgm_ctx *c, const double *X, cudaStream_t st) {
+  if (c->n_tet == 0) return DGM_OK;
+  DGM_DISPATCH(c->p, launch_traces_p, c, X, st)
+}
+
+template <int P>
+static dgm_status launch_energy_p(dgm_ctx *c, const double *E, const double *H, double *out, cudaStream_t st) {
+  const int threads = 256;
+  int64_t grid = (c->n_tet + threads - 1) / threads;
+  if (grid > 4 * (int64_t)c->sms) grid = 4 * (int64_t)c->sms;
+  if (c->n_partial < grid + 1) {
+    cudaFree(c->d_partial);
+    if (cudaMalloc(&c->d_partial, sizeof(double) * (grid + 1)) != cudaSuccess)
+      return set_err(c, DGM_ENOMEM, "energy partials");
+    c->n_partial = grid + 1;
+  }
+  energy_kernel<P><<<(unsigned)grid, threads, 0, st>>>(E, H, c->d_geo, c->progs.norms, c->n_tet, c->d_partial);
+  sum_kernel<<<1, 256, 0, st>>>(c->d_partial, (int)grid, c->d_partial + grid);
+  cudaError_t e = cudaMemcpyAsync(out, c->d_partial + grid, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("energy: ") + cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out, cudaStream_t st) {
+  DGM_DISPATCH(c->p, launch_energy_p, c, E, H, out, st)
+}
+
+int workspace_doubles(int p) {
+  switch (p) {
+    case 1: return Dim<1>::WS;
+    case 2: return Dim<2>::WS;
+    case 3: return Dim<3>::WS;
+    case 4: return Dim<4>::WS;
+    case 5: return Dim<5>::WS;
+    case 6: return Dim<6>::WS;
+    case 7: return Dim<7>::WS;
+    case 8: return Dim<8>::WS;
+    case 9: return Dim<9>::WS;
+    case 10: return Dim<10>::WS;
+  }
+  return 0;
+}
+
+}  // namespace dgm

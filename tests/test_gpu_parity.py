@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA library (through the C ABI) against the oracle on the
+same seeded inputs (SURVEY.md §8(c) G15 metric: max|X_gpu - X_ref| / max|X_ref|
+per field, padding excluded).  Bars (BASELINE.json north_star): <= 1e-12 per
+operator application, <= 1e-10 after the step counts; integer tables bit-exact.
+"""
+import numpy as np
+import pytest
+
+import dgm_inputs as di
+from oracle.mesh import geometry, match_faces
+from oracle.tier_a import TierA
+from oracle.tier_b import TierB
+from oracle.timestep import symplectic_euler
+from oracle import fields
+
+pytestmark = pytest.mark.gpu
+
+TOL_APPLY = 1e-12
+TOL_STEPS = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need CUDA (no CPU fallback exists)"
+    from paper_1104_4208_b200 import load_library
+    load_library()
+
+
+def rel_err(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _problem(n, periodic, p, flux, seed=7, materials=True, jitter=0.1):
+    nx, ny, nz = (n, n, n) if isinstance(n, int) else n
+    m = di.kuhn_mesh(nx, ny, nz, periodic=periodic, jitter=jitter, seed=seed)
+    rng = np.random.default_rng(seed + 100)
+    eps = rng.uniform(1, 4, m.n_tet) if materials else np.ones(m.n_tet)
+    mu = rng.uniform(1, 2, m.n_tet) if materials else np.ones(m.n_tet)
+    rep = m.rep if any(periodic) else None
+    return m, rep, eps, mu
+
+
+def _ctx(m, rep, p, eps, mu, flux):
+    from paper_1104_4208_b200 import Context
+    return Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=flux)
+
+
+CASES = {
+    "pec-central": ((False,) * 3, "central", 2),
+    "periodic-central": ((True,) * 3, "central", 3),
+    "pec-upwind": ((False,) * 3, "upwind", 2),
+    "mixed-upwind": ((False, True, True), "upwind", (2, 3, 3)),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_tables_bit_exact(case):
+    periodic, flux, n = CASES[case]
+    m, rep, eps, mu = _problem(n, periodic, 2, flux)
+    c = _ctx(m, rep, 2, eps, mu, flux)
+    F, detF = geometry(m.xyz, m.tet)
+    for got, want in zip(c.dgm_tables(), match_faces(m.tet, rep, detF)):
+        assert got.dtype == want.dtype and np.array_equal(got, want)
+
+
+def _apply_parity(case, p):
+    periodic, flux, n = CASES[case]
+    m, rep, eps, mu = _problem(n, periodic, p, flux)
+    B = TierB(m.xyz, m.tet, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux)
+    rng = np.random.default_rng(p)
+    E = rng.standard_normal((3, m.n_tet, B.N))
+    H = rng.standard_normal((3, m.n_tet, B.N))
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    dE, dH = c.empty_field(), c.empty_field()
+    c.dgm_apply_curl(Ed, Hd, dE, dH)
+    errs = {"curlE": rel_err(c.to_host(dE), B.dE(E, H, "curl")), "curlH": rel_err(c.to_host(dH), B.dH(E, H, "curl"))}
+    c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
+    errs["allE"] = rel_err(c.to_host(dE), B.dE(E, H))
+    errs["allH"] = rel_err(c.to_host(dH), B.dH(E, H))
+    c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=False)
+    errs["fluxE"] = rel_err(c.to_host(dE), B.dE(E, H, "flux"))
+    errs["fluxH"] = rel_err(c.to_host(dH), B.dH(E, H, "flux"))
+    # padding never written
+    assert float(dE[:, :, B.N:].abs().max() if c.ld > B.N else 0.0) == 0.0
+    return errs
+
+
+@pytest.mark.parametrize("p", list(range(1, 11)))
+def test_apply_parity_all_orders(p):
+    errs = _apply_parity("pec-central", p)
+    assert max(errs.values()) <= TOL_APPLY, errs
+
+
+@pytest.mark.parametrize("case", ["periodic-central", "pec-upwind", "mixed-upwind"])
+@pytest.mark.parametrize("p", [2, 5, 8, 10])
+def test_apply_parity_cases(case, p):
+    errs = _apply_parity(case, p)
+    assert max(errs.values()) <= TOL_APPLY, errs
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("p", [2, 4, 6])
+def test_step_parity_100(case, p):
+    periodic, flux, n = CASES[case]
+    m, rep, eps, mu = _problem(n, periodic, p, flux)
+    B = TierB(m.xyz, m.tet, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux)
+    rng = np.random.default_rng(10 + p)
+    E = rng.standard_normal((3, m.n_tet, B.N)) / (1 + np.arange(B.N)) ** 0.5
+    H = rng.standard_normal((3, m.n_tet, B.N)) / (1 + np.arange(B.N)) ** 0.5
+    dt = 0.02 / (p + 1) ** 2
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    c.dgm_step(Ed, Hd, dt, 100)
+    Er, Hr, _ = symplectic_euler(B, E, H, dt, 100)
+    assert rel_err(c.to_host(Ed), Er) <= TOL_STEPS
+    assert rel_err(c.to_host(Hd), Hr) <= TOL_STEPS
+    assert c.dgm_energy(Ed, Hd) == pytest.approx(B.energy(Er, Hr), rel=1e-13)
+
+
+def test_energy_conserved_central_gpu():
+    """Central flux + PEC: the leapfrog keeps the energy bounded (no drift)."""
+    p = 3
+    m, rep, eps, mu = _problem(2, (False,) * 3, p, "central")
+    c = _ctx(m, rep, p, eps, mu, "central")
+    B = TierB(m.xyz, m.tet, rep, p, eps, mu)
+    rng = np.random.default_rng(0)
+    E = rng.standard_normal((3, m.n_tet, B.N))
+    H = np.zeros_like(E)
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    w0 = c.dgm_energy(Ed, Hd)
+    assert w0 == pytest.approx(B.energy(E, H), rel=1e-13)
+    c.dgm_step(Ed, Hd, 1e-3, 200)
+    assert c.dgm_energy(Ed, Hd) == pytest.approx(w0, rel=0.02)
+
+
+def test_config_c1_vs_tier_a():
+    """C1 end to end: 4³ Kuhn PEC cube, p=2, cavity mode (1,1,0), 10 steps,
+    checked against the definition-level tier-A oracle."""
+    cfg = di.CONFIGS["C1"]
+    m = di.config_mesh("C1")
+    p = cfg["p"]
+    A = TierA(m.xyz, m.tet, None, p, 1.0, 1.0)
+    dt = 0.01
+    E0, _ = fields.cavity110(0.0)
+    _, Hh = fields.cavity110(-0.5 * dt)
+    E = fields.project(m.xyz, m.tet, p, E0)
+    H = fields.project(m.xyz, m.tet, p, Hh)
+    c = _ctx(m, None, p, 1.0, 1.0, "central")
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    c.dgm_step(Ed, Hd, dt, cfg["steps"])
+    Er, Hr, _ = symplectic_euler(A, E, H, dt, cfg["steps"])
+    assert rel_err(c.to_host(Ed), Er) <= TOL_STEPS
+    assert rel_err(c.to_host(Hd), Hr) <= TOL_STEPS
+    # and it is close to the analytic mode (discretisation error, not parity)
+    Ee, _ = fields.cavity110(dt * cfg["steps"])
+    assert np.abs(c.to_host(Ed) - fields.project(m.xyz, m.tet, p, Ee)).max() < 0.05
+
+
+def test_config_c2_full_100_steps():
+    """C2 at full size: 16³ Kuhn periodic (24,576 tets), p=4, plane wave + noise,
+    central, 100 steps, against tier B."""
+    cfg = di.CONFIGS["C2"]
+    m = di.config_mesh("C2")
+    p = cfg["p"]
+    B = TierB(m.xyz, m.tet, m.rep, p, 1.0, 1.0)
+    dt = 1e-3
+    E0, _ = fields.planewave(0.0)
+    _, Hh = fields.planewave(-0.5 * dt)
+    rng = np.random.default_rng(3000 + 2)
+    E = fields.project(m.xyz, m.tet, p, E0) + 1e-3 * rng.standard_normal((3, m.n_tet, B.N))
+    H = fields.project(m.xyz, m.tet, p, Hh) + 1e-3 * rng.standard_normal((3, m.n_tet, B.N))
+    c = _ctx(m, m.rep, p, 1.0, 1.0, "central")
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    c.dgm_step(Ed, Hd, dt, cfg["steps"])
+    Er, Hr, _ = symplectic_euler(B, E, H, dt, cfg["steps"])
+    assert rel_err(c.to_host(Ed), Er) <= TOL_STEPS
+    assert rel_err(c.to_host(Hd), Hr) <= TOL_STEPS
+
+
+def test_bad_inputs_fail_loudly():
+    from paper_1104_4208_b200 import Context, DgmError
+    m = di.kuhn_mesh(2, jitter=0.0)
+    with pytest.raises(DgmError):
+        Context(m.xyz, m.tet, 11)
+    with pytest.raises(DgmError):
+        Context(m.xyz, m.tet[:, ::-1].copy(), 2)     # non-canonical vertex order
+    with pytest.raises(DgmError):
+        Context(m.xyz, m.tet, 2, eps=-1.0)
