@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark of the DG Maxwell hot path (one symplectic-Euler step = one
+H-stage + one E-stage over the whole mesh) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Metric (BASELINE.json): DOF-updates/s per DG time step (FP64) = 6·N·n_tet / step
+time, whole job over all ranks.  Default workload = configs[1] (C2: 16³ Kuhn
+periodic, 24,576 tets, p=4, central flux).  Inputs are resident in HBM when the
+timed region starts; L2 (126 MB) is flushed between timed steps (a 512 MiB
+write), each step is timed with CUDA events on the library's stream.
+`e2e` times the same steps through dgm_step_host (pinned host → device copy of
+E,H, the step, device → host copy of E,H, every step).
+Multi-GPU: the path does not shard in this build (north_star: one GPU), so N>1
+runs N independent replicas ("replicas only"), one per rank.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import dgm_inputs as di  # noqa: E402
+
+METRIC = "DOF-updates/s per DG time step (FP64) and % of HBM/FP64 roofline, 1 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=list(di.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = {}
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_problem(cfg_name):
+    cfg = di.CONFIGS[cfg_name]
+    m = di.config_mesh(cfg_name)
+    eps, mu = di.config_materials(cfg_name, m.n_tet)
+    rep = m.rep if any(cfg["periodic"]) else None
+    p = cfg["p"]
+    # throughput is data independent: seeded C3-recipe coefficients for every config
+    E = di.random_coefficients(m.n_tet, p, 3000 + di.config_index(cfg_name))
+    H = di.random_coefficients(m.n_tet, p, 4000 + di.config_index(cfg_name))
+    return cfg, m, eps, mu, rep, E, H
+
+
+def algorithmic_bytes_per_stage(n_tet, N, upwind):
+    """each stage reads the source field and the updated field
+    and writes the updated field (9N doubles per element), plus per-element
+    metadata (80 B geometry + 16 B nbr + 4 B nbr_face); upwind adds the face
+    metric (96 B) and neighbour impedances."""
+    meta = 80 + 16 + 4 + (96 + 4 * 80 if upwind else 0)
+    return n_tet * (9 * N * 8 + meta)
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_1104_4208_b200 import Context
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    cfg, m, eps, mu, rep, E, H = make_problem(args.config)
+    p = cfg["p"]
+    ctx = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=cfg["flux"])
+    N, n = ctx.N, ctx.n_tet
+    Ed, Hd = ctx.to_device(E), ctx.to_device(H)
+    dt = 1e-4
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        ctx.dgm_step(Ed, Hd, dt, 1)
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    launches = 0
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)          # evict L2 (not timed)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.dgm_step(Ed, Hd, dt, 1)
+            e1.record(stream)
+            launches += ctx.dgm_last_launches()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    t_total = sum(times) / 1e3
+    t_total = dist_max(t_total, world)
+    dof = 6.0 * N * n
+    value = world * dof * args.steps / t_total
+    ms_per_step = 1e3 * t_total / args.steps
+    res = dict(value=value, ms_per_step=ms_per_step, launches=launches, clocks=clk.summary(), N=N, n_tet=n,
+               stage_launches_per_step=ctx.dgm_last_launches())
+    # roofline of the dominant kernel (the stage kernel: 2 launches per central step)
+    upwind = cfg["flux"] == "upwind"
+    nstage = 2
+    # central: the step is exactly 2 stage launches; upwind adds 2 trace launches
+    # (their time is charged to the stage kernel here, a conservative figure)
+    per_launch_s = (t_total / args.steps) / nstage
+    B = algorithmic_bytes_per_stage(n, N, upwind)
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    res["roofline"] = {"bound": "hbm", "achieved": B / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
+                       "frac": (B / per_launch_s / 1e9) / hbm, "traffic": None,
+                       "kernel": "stage_kernel", "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback"}
+    # e2e through dgm_step_host
+    if not args.no_e2e:
+        Eh = torch.empty((3, n, ctx.ld), dtype=torch.float64).pin_memory()
+        Hh = torch.empty((3, n, ctx.ld), dtype=torch.float64).pin_memory()
+        Eh.copy_(Ed.cpu())
+        Hh.copy_(Hd.cpu())
+        ctx.dgm_step_host(Eh, Hh, dt, 1)
+        torch.cuda.synchronize()
+        dist_barrier(world)
+        ts = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.dgm_step_host(Eh, Hh, dt, 1)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        te = dist_max(sum(ts) / 1e3, world)
+        nb = 2 * 3 * n * ctx.ld * 8
+        res["e2e"] = {"value": world * dof * args.steps / te, "unit": "DOF-updates/s",
+                      "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+                      "api": "dgm_step_host (C ABI, pinned host E,H)"}
+    return res, cfg
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def dist_max(x, world):
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(cfg_name, budget_s=20.0):
+    """The oracle (tier B, NumPy/BLAS FP64) timed on the host on a bounded sample:
+    as many full symplectic-Euler steps of the same config as fit in ~budget_s."""
+    import oracle.tier_b as tb
+    cfg, m, eps, mu, rep, E, H = make_problem(cfg_name)
+    p = cfg["p"]
+    t0 = time.perf_counter()
+    B = tb.TierB(m.xyz, m.tet, rep, p, eps, mu, cfg["flux"])
+    setup = time.perf_counter() - t0
+    dt = 1e-4
+    # warm-up step (excluded)
+    H = H + dt * B.dH(E, H)
+    E = E + dt * B.dE(E, H)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        H = H + dt * B.dH(E, H)
+        E = E + dt * B.dE(E, H)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or steps >= 1000:
+            break
+    cores = len(os.sched_getaffinity(0))
+    N = B.N
+    return {"value": 6.0 * N * m.n_tet * steps / el, "unit": "DOF-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"{steps} full symplectic-Euler steps of {cfg_name} ({m.n_tet} tets, p={p}) with oracle tier B "
+                      f"(NumPy+OpenBLAS FP64, {cores} host threads), {el:.1f} s, setup {setup:.1f} s excluded"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        cb = cpu_baseline(args.config, budget_s=max(5.0, min(60.0, 3.0 * args.steps)))
+        cfg = di.CONFIGS[args.config]
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "DOF-updates/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.config, "n_tet": int(np.prod(cfg["n"])) * 6, "p": cfg["p"],
+                           "flux": cfg["flux"]},
+                "cpu_baseline": {k: cb[k] for k in ("kind", "cores", "sample")} | {"value": cb["value"]},
+                "e2e": {"value": cb["value"], "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res, cfg = run_ours(args, rank, world)
+    if rank == 0:
+        line = {"metric": METRIC, "value": res["value"], "unit": "DOF-updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": args.config, "n_tet": res["n_tet"], "p": cfg["p"], "N": res["N"],
+                           "flux": cfg["flux"], "periodic": cfg["periodic"], "l2": "flushed (512 MiB write) between steps",
+                           "parallelism": "replicas only" if world > 1 else "single GPU",
+                           "fields": "seeded random coefficients (C3 recipe); timing is data independent"},
+                "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["launches"]}
+        if "e2e" in res:
+            line["e2e"] = res["e2e"]
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.config)
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
