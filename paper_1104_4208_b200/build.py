@@ -35,13 +35,19 @@ def gen_tables(force=False):
 
 def build(force=False, verbose=False):
     inc = gen_tables(force)
-    srcs = [os.path.join(CSRC, f) for f in ("dgm_host.cpp", "dgm_kernels.cu")]
-    deps = srcs + [inc, os.path.join(CSRC, "dgm_internal.h"), os.path.join(HERE, "..", "include", "dgm.h")]
+    lanedir = os.path.join(CSRC, "lane")
+    os.makedirs(lanedir, exist_ok=True)
+    from .gen import lanegen
+    if force or _stale(os.path.join(lanedir, "lane_p4.cuh"), [os.path.join(HERE, "gen", "lanegen.py"), inc]):
+        lanegen.emit_all(lanedir, 4)
+    srcs = [os.path.join(CSRC, f) for f in ("dgm_host.cpp", "dgm_kernels.cu", "dgm_lane.cu")]
+    deps = srcs + [inc, os.path.join(CSRC, "dgm_internal.h"), os.path.join(HERE, "..", "include", "dgm.h"),
+                   os.path.join(lanedir, "lane_p4.cuh")]
     if not force and not _stale(LIB, deps):
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-x", "cu", srcs[0], "-x", "cu", srcs[1],
+           "-Xptxas", "-v" if verbose else "-O3", "-x", "cu", srcs[0], "-x", "cu", srcs[1], "-x", "cu", srcs[2],
            "-o", LIB, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -81,6 +81,7 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_fmet);
   cudaFree(c->d_blob);
   cudaFree(c->d_trX);
+  for (int i = 0; i < 4; ++i) cudaFree(c->d_tr[i]);
   cudaFree(c->d_partial);
   cudaFree(c->d_E);
   cudaFree(c->d_H);
@@ -254,6 +255,8 @@ dgm_status upload_impl(dgm_ctx *c) {
     CUDA_TRY(c, cudaMemcpy(c->d_fmet, c->h_fmet.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice));
     CUDA_TRY(c, cudaMalloc(&c->d_trX, sizeof(double) * n * 8 * c->NF));
   }
+  if (c->p <= dgm::kLanePmax)
+    for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * n * 8 * c->NF));
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
   for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);
@@ -317,6 +320,13 @@ dgm_status dgm_apply_curl(dgm_ctx *c, const double *E, const double *H, double *
   if (!c || !E || !H) return dgm::set_err(c, DGM_EINVAL, "null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   c->launches = 0;
+  if (c->p <= dgm::kLanePmax) {
+    dgm_status s = DGM_OK;
+    if (dE) s = dgm::launch_lane_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
+    if (s == DGM_OK && dH)
+      s = dgm::launch_lane_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
+    return s;
+  }
   if (dE) {
     dgm_status s = dgm::launch_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, st);
     if (s != DGM_OK) return s;
@@ -331,6 +341,14 @@ dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *
   cudaStream_t st = (cudaStream_t)stream;
   int om = accumulate ? dgm::OUT_ACCUM : dgm::OUT_WRITE;
   c->launches = 0;
+  if (c->p <= dgm::kLanePmax) {
+    double *TE = c->d_tr[0], *TH = c->d_tr[2];
+    dgm_status s = dgm::launch_lane_traces(c, E, TE, st);
+    if (s == DGM_OK) s = dgm::launch_lane_traces(c, H, TH, st);
+    if (s == DGM_OK && dE) s = dgm::launch_lane_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, TH, TE, nullptr, st);
+    if (s == DGM_OK && dH) s = dgm::launch_lane_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, TE, TH, nullptr, st);
+    return s;
+  }
   if (dE) {
     if (c->flux == DGM_FLUX_UPWIND) {
       dgm_status s = dgm::launch_traces(c, E, st);
@@ -353,6 +371,25 @@ dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps,
   if (!c || !E || !H || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
   cudaStream_t st = (cudaStream_t)stream;
   c->launches = 0;
+  if (nsteps == 0) return DGM_OK;
+  if (c->p <= dgm::kLanePmax) {
+    // traces of the field each stage reads from its neighbours are produced by the
+    // stage that updated it; recomputed at entry so that resume is exact.
+    const bool up = c->flux == DGM_FLUX_UPWIND;
+    int ce = 0, ch = 0;
+    dgm_status r = dgm::launch_lane_traces(c, E, c->d_tr[0], st);
+    if (r == DGM_OK && up) r = dgm::launch_lane_traces(c, H, c->d_tr[2], st);
+    for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
+      double *TE = c->d_tr[ce], *THr = c->d_tr[2 + ch], *THw = c->d_tr[2 + (up ? 1 - ch : ch)];
+      r = dgm::launch_lane_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
+      if (up) ch = 1 - ch;
+      if (r != DGM_OK) break;
+      double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
+      r = dgm::launch_lane_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
+      if (up) ce = 1 - ce;
+    }
+    return r;
+  }
   for (int64_t s = 0; s < nsteps; ++s) {
     dgm_status r;
     if (c->flux == DGM_FLUX_UPWIND && (r = dgm::launch_traces(c, H, st)) != DGM_OK) return r;

@@ -85,7 +85,8 @@ struct dgm_ctx {
   double *d_fmet = nullptr;
   void *d_blob = nullptr;
   dgm::DevProgs progs{};
-  double *d_trX = nullptr;     // upwind trace buffer
+  double *d_trX = nullptr;     // upwind trace buffer (warp path)
+  double *d_tr[4] = {nullptr, nullptr, nullptr, nullptr};  // lane path: TE0, TE1, TH0, TH1
   double *d_partial = nullptr; // energy partial sums
   int64_t n_partial = 0;
   double *d_E = nullptr, *d_H = nullptr;   // device copies for dgm_step_host
@@ -101,4 +102,10 @@ dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, doubl
 dgm_status launch_traces(dgm_ctx *c, const double *X, cudaStream_t st);
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
 int workspace_doubles(int p);
+// lane-per-element path (dgm_lane.cu), p <= kLanePmax
+constexpr int kLanePmax = 4;
+dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
+                             int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
+                             cudaStream_t st);
+dgm_status launch_lane_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 }  // namespace dgm
