@@ -256,7 +256,8 @@ dgm_status upload_impl(dgm_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->d_trX, sizeof(double) * n * 8 * c->NF));
   }
   if (c->p <= dgm::kLanePmax)
-    for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * n * 8 * c->NF));
+    for (int i = 0; i < 4; ++i)   // groups of 16 elements interleaved: round up
+      CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * ((n + 15) / 16 * 16) * 8 * c->NF));
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
   for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);

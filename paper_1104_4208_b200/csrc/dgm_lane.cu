@@ -1,15 +1,19 @@
-// Lane-per-element stage kernels for low orders (p <= DGM_LANE_PMAX), sm_100a FP64.
+// Lane-pair stage kernels for low orders (p <= kLanePmax), sm_100a FP64.
 //
-// A warp owns 32 consecutive elements.  Their coefficient blocks are contiguous
-// in the SoA field arrays, so they are loaded/stored with fully coalesced
-// accesses and transposed through shared memory into an element-interleaved
-// layout s[slot*33 + lane] (conflict-free for the compute).  Every thread then
-// runs the same generated straight-line program (gen/lanegen.py) on its own
-// element: curl by the recurrence sweeps, traces, numerical flux, lift, inverse
-// mass, update — coefficients are compile-time constants (warp-uniform).
-// Neighbour traces come from a trace buffer tr[e][f][k][γ] that the previous
-// stage wrote for the field it updated (the stage that updates X also emits
-// X's traces), so no neighbour volume data is read.
+// A warp owns 16 consecutive elements; lanes e and e+16 form the pair that
+// works on element e0+e (half h = lane>>4).  The elements' coefficient blocks
+// are contiguous in the SoA arrays, so they move with fully coalesced accesses
+// into shared memory with an element-major layout s[e*SE + slot], SE odd (the 16
+// lanes of a half-warp then hit 16 distinct bank pairs).  Both halves run the same generated code (gen/lanegen.py) on
+// different components, so there is no divergence:
+//   curl     ∂x: (Ŷz → -ĉy | Ŷy → +ĉz)  ∂y: (Ŷz → +ĉx | Ŷx → -ĉz)  ∂z: (Ŷy → -ĉx | Ŷx → +ĉy)
+//   traces   half h: a_h = Ŷ·t̂_h on each face
+//   lift     half 0: B = sf D₁ (+ upwind), half 1: A = -sf D₂ (+ upwind);
+//            acc_m += t̂1_m L_f(A) + t̂2_m L_f(B)
+// Own and neighbour traces come from a trace buffer written by the stage that
+// updated that field (no neighbour volume reads).  Its layout interleaves groups
+// of 16 elements, tr[e/16][f][k][γ][e%16], so the own-trace loads and the
+// trace stores of a half-warp are single 128-byte transactions.
 #include <cstdint>
 
 #include "dgm_internal.h"
@@ -20,273 +24,347 @@
 
 namespace dgm {
 
-constexpr int kLS = 33;   // interleave stride (doubles)
+__host__ __device__ constexpr int odd_up(int x) { return x | 1; }
 
 template <int P>
-struct LDim {
+struct L2 {
   static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
   static constexpr int NF = (P + 1) * (P + 2) / 2;
   static constexpr int LD = (N + 3) & ~3;
-  static constexpr int SY = 3 * N;                               // Y, then X (or dX) staging
-  static constexpr int SA = 3 * N > 8 * NF ? 3 * N : 8 * NF;    // accumulator, then X-traces
-  static constexpr int WS = (SY + SA) * kLS;                     // doubles per warp
+  static constexpr int SY = 0, SA = 3 * N;
+  static constexpr int SE = odd_up(6 * N);         // per-element stride (odd: conflict-free)
+  static constexpr int WS = 16 * SE;               // doubles per warp
+  static constexpr int J = (16 * LD + 31) / 32;    // 8-byte copies per lane per component
   static constexpr int WARPS_RAW = (200 * 1024) / (WS * 8);
-  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 4 ? 4 : WARPS_RAW);
+  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
 };
 
-#define DGM_LANE_OPS(P)                                                                                    \
-  template <>                                                                                              \
-  struct LaneOps<P> {                                                                                      \
-    static constexpr int NF = LDim<P>::NF;                                                                 \
-    static __device__ __forceinline__ void curl(const double *sY, double *sA) { lane_curl_p##P(sY, sA); }  \
-    template <int F>                                                                                       \
-    static __device__ __forceinline__ void trace(const double *sY, double (&t)[2][NF]) {                   \
-      if (F == 0) lane_trace_p##P##_f0(sY, t);                                                             \
-      else if (F == 1) lane_trace_p##P##_f1(sY, t);                                                        \
-      else if (F == 2) lane_trace_p##P##_f2(sY, t);                                                        \
-      else lane_trace_p##P##_f3(sY, t);                                                                    \
-    }                                                                                                      \
-    template <int F>                                                                                       \
-    static __device__ __forceinline__ void lift(const double (&q)[3][NF], double *sA) {                    \
-      if (F == 0) lane_lift_p##P##_f0(q, sA);                                                              \
-      else if (F == 1) lane_lift_p##P##_f1(q, sA);                                                         \
-      else if (F == 2) lane_lift_p##P##_f2(q, sA);                                                         \
-      else lane_lift_p##P##_f3(q, sA);                                                                     \
-    }                                                                                                      \
+#define DGM_L2_OPS(P)                                                                                     \
+  template <>                                                                                             \
+  struct LOps<P> {                                                                                        \
+    static __device__ __forceinline__ void sweep(int d, const double *src, double *dst, double sgn) {     \
+      if (d == 0) lane_sweep_p##P##_d0(src, dst, sgn);                                                    \
+      else if (d == 1) lane_sweep_p##P##_d1(src, dst, sgn);                                               \
+      else lane_sweep_p##P##_d2(src, dst, sgn);                                                           \
+    }                                                                                                     \
+    static __device__ __forceinline__ void trace(int f, const double *a, const double *b, double *out,    \
+                                                 int os) {                                                \
+      if (f == 0) lane_trace_p##P##_f0(a, b, out, os);                                                    \
+      else if (f == 1) lane_trace_p##P##_f1(a, out, os);                                                  \
+      else if (f == 2) lane_trace_p##P##_f2(a, out, os);                                                  \
+      else lane_trace_p##P##_f3(a, out, os);                                                              \
+    }                                                                                                     \
+    template <int NF>                                                                                     \
+    static __device__ __forceinline__ void lift(int f, const double (&q)[NF], double *o, double *o0,      \
+                                                int h) {                                                  \
+      lane_lift_p##P(f, q, o, o0, h);                                                                     \
+    }                                                                                                     \
   };
 
 template <int P>
-struct LaneOps;
-DGM_LANE_OPS(1)
-DGM_LANE_OPS(2)
-DGM_LANE_OPS(3)
-DGM_LANE_OPS(4)
+struct LOps;
+DGM_L2_OPS(1)
+DGM_L2_OPS(2)
+DGM_L2_OPS(3)
+DGM_L2_OPS(4)
 
-__device__ __constant__ double kLT1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
-__device__ __constant__ double kLT2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
+// tangential component h of face f: a_h = Y[c] (- Y[0] on face 0)
+__device__ __forceinline__ int tang_comp(int f, int h) {
+  return f == 0 ? 1 + h : (f == 1 ? 1 + h : (f == 2 ? 2 * h : h));
+}
+// lift destination component of half h on faces 1..3 (t̂ entries are +1 there)
+__device__ __forceinline__ int lift_dst(int f, int h) {
+  return f == 1 ? (h ? 1 : 2) : (f == 2 ? (h ? 0 : 2) : (h ? 0 : 1));
+}
 
-// coalesced load of `rows` contiguous blocks of LD doubles (component stride cs)
-// into the interleaved layout s[(c*N + b)*33 + e]
-template <int N, int LD>
-__device__ __forceinline__ void lane_load(const double *__restrict__ F, int64_t e0, int nel, int64_t cs, double *s,
-                                          int lane) {
+__device__ __forceinline__ void cp_async8(double *smem_dst, const double *gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Per-lane destination offsets of the flat copy of 16 element blocks (16*LD
+// contiguous doubles per component): flat index i = lane + 32 j -> element i/LD,
+// mode i%LD; -1 marks padding modes.  Computed once per kernel.
+template <int N, int LD, int SE, int J>
+struct CopyMap {
+  int off[J];
+  __device__ __forceinline__ CopyMap(int lane) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int i = lane + 32 * j, e = i / LD, b = i - e * LD;
+      off[j] = (b < N && e < 16) ? e * SE + b : -1;
+    }
+  }
+};
+
+// Coalesced asynchronous load (cp.async, LDGSTS) of nel contiguous element blocks
+// per component into s[e*SE + c*N + b]; every copy of the group is in flight at once;
+// the caller waits with cp_async_wait_all + __syncwarp.
+template <int N, int LD, int SE, int J>
+__device__ __forceinline__ void l2_load_async(const CopyMap<N, LD, SE, J> &m, const double *__restrict__ F,
+                                              int64_t e0, int nel, int64_t cs, double *s, int lane) {
+  const int lim = nel * LD;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double *src = F + c * cs + e0 * LD;
-    for (int i = lane; i < nel * LD; i += 32) {
-      const int e = i / LD, b = i - e * LD;
-      if (b < N) s[(c * N + b) * kLS + e] = __ldg(src + i);
-    }
+    const double *src = F + c * cs + e0 * LD + lane;
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (m.off[j] >= 0 && lane + 32 * j < lim) cp_async8(s + c * N + m.off[j], src + 32 * j);
   }
 }
 
-template <int N, int LD>
-__device__ __forceinline__ void lane_store(double *__restrict__ F, int64_t e0, int nel, int64_t cs, const double *s,
-                                           int lane, bool accumulate) {
+template <int N, int LD, int SE, int J>
+__device__ __forceinline__ void l2_load(const CopyMap<N, LD, SE, J> &m, const double *__restrict__ F, int64_t e0,
+                                        int nel, int64_t cs, double *s, int lane) {
+  l2_load_async(m, F, e0, nel, cs, s, lane);
+  cp_async_wait_all();
+}
+
+template <int N, int LD, int SE, int J>
+__device__ __forceinline__ void l2_store(const CopyMap<N, LD, SE, J> &m, double *__restrict__ F, int64_t e0, int nel,
+                                         int64_t cs, const double *s, int lane, bool accumulate) {
+  const int lim = nel * LD;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double *dst = F + c * cs + e0 * LD;
-    for (int i = lane; i < nel * LD; i += 32) {
-      const int e = i / LD, b = i - e * LD;
-      if (b < N) {
-        const double v = s[(c * N + b) * kLS + e];
-        dst[i] = accumulate ? dst[i] + v : v;
+    double *dst = F + c * cs + e0 * LD + lane;
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (m.off[j] >= 0 && lane + 32 * j < lim) {
+        const double v = s[c * N + m.off[j]];
+        dst[32 * j] = accumulate ? dst[32 * j] + v : v;
       }
-    }
   }
 }
 
-// traces of the interleaved field in sV (this lane's column) -> interleaved sT[(f*2+k)*NF + γ]
-template <int P>
-__device__ __forceinline__ void lane_traces_all(const double *sV, double *sT) {
-  constexpr int NF = LDim<P>::NF;
-  double t[2][NF];
-  LaneOps<P>::template trace<0>(sV, t);
-#pragma unroll
-  for (int g = 0; g < NF; ++g) { sT[(0 * NF + g) * kLS] = t[0][g]; sT[(1 * NF + g) * kLS] = t[1][g]; }
-  LaneOps<P>::template trace<1>(sV, t);
-#pragma unroll
-  for (int g = 0; g < NF; ++g) { sT[(2 * NF + g) * kLS] = t[0][g]; sT[(3 * NF + g) * kLS] = t[1][g]; }
-  LaneOps<P>::template trace<2>(sV, t);
-#pragma unroll
-  for (int g = 0; g < NF; ++g) { sT[(4 * NF + g) * kLS] = t[0][g]; sT[(5 * NF + g) * kLS] = t[1][g]; }
-  LaneOps<P>::template trace<3>(sV, t);
-#pragma unroll
-  for (int g = 0; g < NF; ++g) { sT[(6 * NF + g) * kLS] = t[0][g]; sT[(7 * NF + g) * kLS] = t[1][g]; }
-}
-
-// coalesced store of the interleaved traces of 32 elements to tr[e][8NF]
+// trace-buffer index of (element ge, face f, component k, mode γ): groups of 16
+// elements interleaved, tr[ge/16][f][k][γ][ge%16]
 template <int NF>
-__device__ __forceinline__ void lane_store_traces(double *__restrict__ tr, int64_t e0, int nel, const double *sT,
-                                                  int lane) {
-  double *dst = tr + e0 * 8 * NF;
-  for (int i = lane; i < nel * 8 * NF; i += 32) {
-    const int e = i / (8 * NF), r = i - e * 8 * NF;
-    dst[i] = sT[r * kLS + e];
-  }
+__device__ __forceinline__ int64_t tix(int64_t ge, int f, int k, int g) {
+  return (((ge >> 4) * 8 * NF + (f * 2 + k) * NF + g) << 4) + (ge & 15);
 }
 
-template <int P, int F>
-__device__ __forceinline__ void lane_face(const StageArgs &a, const double *trY, const double *sYl, double *sAl,
-                                          int64_t e, const Geo &g, bool stageE, double sgn) {
-  constexpr int NF = LDim<P>::NF;
-  double t[2][NF];
-  LaneOps<P>::template trace<F>(sYl, t);
-  const int nb = a.nbr[4 * e + F];
-  const int gf = a.nbrf[4 * e + F];
-  double w = 0.5, k = 0.0;
-  if (a.upwind) {
-    const double Zm = g.Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
-    if (stageE) {
-      w = Zp / (Zm + Zp);
-      k = 1.0 / (Zm + Zp);
-    } else {
-      const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
-      w = Yp / (Ym + Yp);
-      k = 1.0 / (Ym + Yp);
-    }
-  }
-  const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
-  const double sf = (F & 1) ? -1.0 : 1.0;
-  const double *tn = nb >= 0 ? trY + ((int64_t)nb * 4 + gf) * 2 * NF : nullptr;
-  double q[3][NF];
-#pragma unroll
-  for (int gm = 0; gm < NF; ++gm) {
-    const double yn1 = nb >= 0 ? __ldg(tn + gm) : mirrorY * t[0][gm];
-    const double yn2 = nb >= 0 ? __ldg(tn + NF + gm) : mirrorY * t[1][gm];
-    const double d1 = w * (yn1 - t[0][gm]), d2 = w * (yn2 - t[1][gm]);
-#pragma unroll
-    for (int m = 0; m < 3; ++m) q[m][gm] = sf * (d1 * kLT2[F][m] - d2 * kLT1[F][m]);
-  }
-  if (a.upwind) {
-    const double *to = a.trX + ((int64_t)e * 4 + F) * 2 * NF;
-    const double *tx = nb >= 0 ? a.trX + ((int64_t)nb * 4 + gf) * 2 * NF : nullptr;
-    const double *M = a.fmet + 12 * e + 3 * F;
-    const double M0 = M[0], M1 = M[1], M2 = M[2];
-    const double ps = (stageE ? 1.0 : -1.0) * sgn;
-#pragma unroll
-    for (int gm = 0; gm < NF; ++gm) {
-      const double xo1 = __ldg(to + gm), xo2 = __ldg(to + NF + gm);
-      const double xn1 = nb >= 0 ? __ldg(tx + gm) : mirrorX * xo1;
-      const double xn2 = nb >= 0 ? __ldg(tx + NF + gm) : mirrorX * xo2;
-      const double j1 = k * (xn1 - xo1), j2 = k * (xn2 - xo2);
-      const double p1 = j1 * M0 + j2 * M1, p2 = j1 * M1 + j2 * M2;
-#pragma unroll
-      for (int m = 0; m < 3; ++m) q[m][gm] += ps * (p1 * kLT1[F][m] + p2 * kLT2[F][m]);
-    }
-  }
-  LaneOps<P>::template lift<F>(q, sAl);
-}
-
+// traces of this lane's element (slots [0,3N)): tangential component h of all 4
+// faces, written straight to the (interleaved, coalesced) trace buffer
 template <int P>
-__global__ void __launch_bounds__(LDim<P>::WARPS * 32)
+__device__ __forceinline__ void l2_traces_out(const double *el, int h, double *__restrict__ tr, int64_t ge) {
+  using D = L2<P>;
+#pragma unroll 1
+  for (int f = 0; f < 4; ++f) {
+    const int c = tang_comp(f, h);
+    LOps<P>::trace(f, el + c * D::N, el, tr + tix<D::NF>(ge, f, h, 0), 16);
+  }
+}
+
+template <int P, bool UP>
+__global__ void __launch_bounds__(L2<P>::WARPS * 32)
     lane_stage_kernel(StageArgs a, const double *__restrict__ trY, double *__restrict__ trOut) {
-  using D = LDim<P>;
+  using D = L2<P>;
   constexpr int N = D::N, NF = D::NF, LD = D::LD;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *sY = smem + warp * D::WS;
-  double *sA = sY + D::SY * kLS;
+  const int e = lane & 15, h = lane >> 4;
+  double *sw = smem + warp * D::WS;
+  double *el = sw + e * D::SE;
+  const CopyMap<N, LD, D::SE, D::J> cmap(lane);
   const int64_t cs = a.n_tet * LD;
   const bool stageE = a.stage == STAGE_E;
-  for (int64_t e0 = ((int64_t)blockIdx.x * D::WARPS + warp) * 32; e0 < a.n_tet;
-       e0 += (int64_t)gridDim.x * D::WARPS * 32) {
-    const int nel = (int)(a.n_tet - e0 < 32 ? a.n_tet - e0 : 32);
-    const bool active = lane < nel;
-    const int64_t e = e0 + lane;
-    lane_load<N, LD>(a.Y, e0, nel, cs, sY, lane);
+  const bool upd = a.out_mode == OUT_UPDATE;
+  // curl split: (source comp, destination comp, sign) per direction and half
+  const int csrc0 = h ? 1 : 2, cdst0 = h ? 2 : 1;   // ∂x: (Ŷz → -ĉy | Ŷy → +ĉz)
+  const int csrc1 = h ? 0 : 2, cdst1 = h ? 2 : 0;   // ∂y: (Ŷz → +ĉx | Ŷx → -ĉz)
+  const int csrc2 = h ? 0 : 1, cdst2 = h ? 1 : 0;   // ∂z: (Ŷy → -ĉx | Ŷx → +ĉy)
+  const double cs0 = h ? 1.0 : -1.0, cs1 = h ? -1.0 : 1.0, cs2 = h ? 1.0 : -1.0;
+  for (int64_t e0 = ((int64_t)blockIdx.x * D::WARPS + warp) * 16; e0 < a.n_tet;
+       e0 += (int64_t)gridDim.x * D::WARPS * 16) {
+    const int nel = (int)(a.n_tet - e0 < 16 ? a.n_tet - e0 : 16);
+    const bool active = e < nel;
+    const int64_t ge = e0 + e;
+    l2_load(cmap, a.Y, e0, nel, cs, sw, lane);
+    for (int i = h; i < 3 * N; i += 2) el[D::SA + i] = 0.0;
     __syncwarp();
-    double *sYl = sY + lane, *sAl = sA + lane;
     if (a.do_curl) {
-      LaneOps<P>::curl(sYl, sAl);
-    } else {
-#pragma unroll 4
-      for (int i = 0; i < 3 * N; ++i) sAl[i * kLS] = 0.0;
+      LOps<P>::sweep(0, el + csrc0 * N, el + D::SA + cdst0 * N, cs0);
+      __syncwarp();
+      LOps<P>::sweep(1, el + csrc1 * N, el + D::SA + cdst1 * N, cs1);
+      __syncwarp();
+      LOps<P>::sweep(2, el + csrc2 * N, el + D::SA + cdst2 * N, cs2);
+      __syncwarp();
     }
-    if (a.do_flux && active) {
-      const Geo g = a.geo[e];
-      const double sgn = g.detF > 0 ? 1.0 : -1.0;
-      lane_face<P, 0>(a, trY, sYl, sAl, e, g, stageE, sgn);
-      lane_face<P, 1>(a, trY, sYl, sAl, e, g, stageE, sgn);
-      lane_face<P, 2>(a, trY, sYl, sAl, e, g, stageE, sgn);
-      lane_face<P, 3>(a, trY, sYl, sAl, e, g, stageE, sgn);
+    bool x_issued = false;
+    if (a.do_flux) {
+      Geo g;
+      double sgn = 1.0;
+      if (active) {
+        g = a.geo[ge];
+        sgn = g.detF > 0 ? 1.0 : -1.0;
+      }
+      const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
+      // own and neighbour traces of this half's component (written by the stage that
+      // last updated Ŷ), prefetched one face ahead
+      double ownv[NF], nbv[NF];
+      auto fetch = [&](int f) {
+        if (!active) return;
+        const double *to = trY + tix<NF>(ge, f, h, 0);
+#pragma unroll
+        for (int gm = 0; gm < NF; ++gm) ownv[gm] = __ldg(to + 16 * gm);
+        const int nb = a.nbr[4 * ge + f];
+        if (nb >= 0) {
+          const double *tn = trY + tix<NF>(nb, a.nbrf[4 * ge + f], h, 0);
+#pragma unroll
+          for (int gm = 0; gm < NF; ++gm) nbv[gm] = __ldg(tn + 16 * gm);
+        }
+      };
+      fetch(0);
+      if (upd) {
+        // the curl is done with Ŷ (and the fluxes only need traces): fetch X into
+        // its slots now so the copy overlaps the four face fluxes and lifts
+        l2_load_async(cmap, a.X, e0, nel, cs, sw, lane);
+        x_issued = true;
+      }
+#pragma unroll 1
+      for (int f = 0; f < 4; ++f) {
+        double q[NF], cur[NF];
+#pragma unroll
+        for (int gm = 0; gm < NF; ++gm) {
+          q[gm] = ownv[gm];
+          cur[gm] = nbv[gm];
+        }
+        if (f < 3) fetch(f + 1);
+        if (active) {
+          const int nb = a.nbr[4 * ge + f];
+          const int gf = a.nbrf[4 * ge + f];
+          double w = 0.5, k = 0.0;
+          if (UP) {
+            const double Zm = g.Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
+            if (stageE) {
+              w = Zp / (Zm + Zp);
+              k = 1.0 / (Zm + Zp);
+            } else {
+              const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
+              w = Yp / (Ym + Yp);
+              k = 1.0 / (Ym + Yp);
+            }
+          }
+          const double sf = (f & 1) ? -1.0 : 1.0;
+          const double fs = h ? -sf : sf;   // half 0: B = sf D1, half 1: A = -sf D2
+          double M0 = 0, M1 = 0, M2 = 0, ps = 0;
+          const double *xo = nullptr, *xn = nullptr;
+          if (UP) {
+            const double *M = a.fmet + 12 * ge + 3 * f;
+            M0 = M[0], M1 = M[1], M2 = M[2];
+            ps = (stageE ? 1.0 : -1.0) * sgn;
+            xo = a.trX + tix<NF>(ge, f, 0, 0);
+            xn = nb >= 0 ? a.trX + tix<NF>(nb, gf, 0, 0) : nullptr;
+          }
+#pragma unroll
+          for (int gm = 0; gm < NF; ++gm) {
+            const double t = q[gm];
+            const double tnv = nb >= 0 ? cur[gm] : mirrorY * t;
+            double v = fs * w * (tnv - t);
+            if (UP) {
+              const double xo1 = __ldg(xo + 16 * gm), xo2 = __ldg(xo + 16 * (NF + gm));
+              const double xn1 = nb >= 0 ? __ldg(xn + 16 * gm) : mirrorX * xo1;
+              const double xn2 = nb >= 0 ? __ldg(xn + 16 * (NF + gm)) : mirrorX * xo2;
+              const double j1 = k * (xn1 - xo1), j2 = k * (xn2 - xo2);
+              v += ps * (h ? (j1 * M0 + j2 * M1) : (j1 * M1 + j2 * M2));
+            }
+            q[gm] = v;
+          }
+        }
+        // face 0: t̂1 = (-1,1,0), t̂2 = (-1,0,1): acc1 += A, acc2 += B, acc0 -= A+B;
+        // faces 1-3: one destination component per half
+        const int dst = f == 0 ? (h ? 1 : 2) : lift_dst(f, h);
+        LOps<P>::lift(f, q, el + D::SA + dst * N, el + D::SA, h);
+        __syncwarp();
+      }
     }
-    __syncwarp();
-    // S2 + S6: inverse mass with geometry; the sY area now stages X (or dX)
-    const bool upd = a.out_mode == OUT_UPDATE;
-    if (upd) lane_load<N, LD>(a.X, e0, nel, cs, sY, lane);
+    // S2 + S6: inverse mass with geometry, update or write; slots [0,3N) stage X / dX
+    if (upd) {
+      if (x_issued) {
+        cp_async_wait_all();
+      } else {
+        __syncwarp();
+        l2_load(cmap, a.X, e0, nel, cs, sw, lane);
+      }
+    }
     __syncwarp();
     if (active) {
-      const Geo g = a.geo[e];
+      const Geo g = a.geo[ge];
       const double cm = stageE ? g.inv_eps : -g.inv_mu;
       const double sc = upd ? a.dt * cm : cm;
-      for (int b = 0; b < N; ++b) {
-        const double v0 = sAl[b * kLS], v1 = sAl[(N + b) * kLS], v2 = sAl[(2 * N + b) * kLS];
+      for (int b = h; b < N; b += 2) {
+        const double v0 = el[D::SA + b], v1 = el[D::SA + N + b], v2 = el[D::SA + 2 * N + b];
         const double x0 = sc * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
         const double x1 = sc * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
         const double x2 = sc * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
         if (upd) {
-          sYl[b * kLS] += x0;
-          sYl[(N + b) * kLS] += x1;
-          sYl[(2 * N + b) * kLS] += x2;
+          el[b] += x0;
+          el[N + b] += x1;
+          el[2 * N + b] += x2;
         } else {
-          sYl[b * kLS] = x0;
-          sYl[(N + b) * kLS] = x1;
-          sYl[(2 * N + b) * kLS] = x2;
+          el[b] = x0;
+          el[N + b] = x1;
+          el[2 * N + b] = x2;
         }
       }
     }
     __syncwarp();
     if (upd) {
-      lane_store<N, LD>(a.X, e0, nel, cs, sY, lane, false);
-      if (trOut) {
-        // traces of the updated field for the next stage's neighbours
-        lane_traces_all<P>(sYl, sAl);
-        __syncwarp();
-        lane_store_traces<NF>(trOut, e0, nel, sA, lane);
-      }
+      l2_store(cmap, a.X, e0, nel, cs, sw, lane, false);
+      if (trOut && active) l2_traces_out<P>(el, h, trOut, ge);
     } else {
-      lane_store<N, LD>(a.dX, e0, nel, cs, sY, lane, a.out_mode == OUT_ACCUM);
+      l2_store(cmap, a.dX, e0, nel, cs, sw, lane, a.out_mode == OUT_ACCUM);
     }
     __syncwarp();
   }
 }
 
 template <int P>
-__global__ void __launch_bounds__(LDim<P>::WARPS * 32)
+__global__ void __launch_bounds__(L2<P>::WARPS * 32)
     lane_trace_kernel(const double *__restrict__ X, double *__restrict__ tr, int64_t n_tet) {
-  using D = LDim<P>;
+  using D = L2<P>;
   constexpr int N = D::N, NF = D::NF, LD = D::LD;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *sY = smem + warp * D::WS;
-  double *sA = sY + D::SY * kLS;
+  const int e = lane & 15, h = lane >> 4;
+  double *sw = smem + warp * D::WS;
+  const CopyMap<N, LD, D::SE, D::J> cmap(lane);
   const int64_t cs = n_tet * LD;
-  for (int64_t e0 = ((int64_t)blockIdx.x * D::WARPS + warp) * 32; e0 < n_tet; e0 += (int64_t)gridDim.x * D::WARPS * 32) {
-    const int nel = (int)(n_tet - e0 < 32 ? n_tet - e0 : 32);
-    lane_load<N, LD>(X, e0, nel, cs, sY, lane);
+  for (int64_t e0 = ((int64_t)blockIdx.x * D::WARPS + warp) * 16; e0 < n_tet; e0 += (int64_t)gridDim.x * D::WARPS * 16) {
+    const int nel = (int)(n_tet - e0 < 16 ? n_tet - e0 : 16);
+    l2_load(cmap, X, e0, nel, cs, sw, lane);
     __syncwarp();
-    lane_traces_all<P>(sY + lane, sA + lane);
-    __syncwarp();
-    lane_store_traces<NF>(tr, e0, nel, sA, lane);
+    if (e < nel) l2_traces_out<P>(sw + e * D::SE, h, tr, e0 + e);
     __syncwarp();
   }
 }
 
+template <typename K>
+static int occupancy_grid(dgm_ctx *c, K kernel, int warps, size_t smem, int64_t groups) {
+  int occ = 0;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, warps * 32, smem);
+  if (occ < 1) occ = 1;
+  int64_t grid = (groups + warps - 1) / warps;
+  if (grid > (int64_t)c->sms * occ) grid = (int64_t)c->sms * occ;
+  return (int)grid;
+}
+
 template <int P>
 static dgm_status lane_stage_p(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
-  using D = LDim<P>;
+  using D = L2<P>;
   const size_t smem = sizeof(double) * D::WS * D::WARPS;
-  static int occ = -1;
-  if (occ < 0) {
-    cudaFuncSetAttribute(lane_stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_stage_kernel<P>, D::WARPS * 32, smem);
-    if (occ < 1) occ = 1;
+  if (a.upwind) {
+    const int grid = occupancy_grid(c, lane_stage_kernel<P, true>, D::WARPS, smem, (c->n_tet + 15) / 16);
+    lane_stage_kernel<P, true><<<grid, D::WARPS * 32, smem, st>>>(a, trY, trOut);
+  } else {
+    const int grid = occupancy_grid(c, lane_stage_kernel<P, false>, D::WARPS, smem, (c->n_tet + 15) / 16);
+    lane_stage_kernel<P, false><<<grid, D::WARPS * 32, smem, st>>>(a, trY, trOut);
   }
-  const int64_t groups = (c->n_tet + 31) / 32;
-  int64_t grid = (groups + D::WARPS - 1) / D::WARPS;
-  if (grid > (int64_t)c->sms * occ) grid = (int64_t)c->sms * occ;
-  lane_stage_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(a, trY, trOut);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("lane_stage_kernel: ") + cudaGetErrorString(e));
@@ -295,18 +373,10 @@ static dgm_status lane_stage_p(dgm_ctx *c, const StageArgs &a, const double *trY
 
 template <int P>
 static dgm_status lane_trace_p(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
-  using D = LDim<P>;
+  using D = L2<P>;
   const size_t smem = sizeof(double) * D::WS * D::WARPS;
-  static int occ = -1;
-  if (occ < 0) {
-    cudaFuncSetAttribute(lane_trace_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lane_trace_kernel<P>, D::WARPS * 32, smem);
-    if (occ < 1) occ = 1;
-  }
-  const int64_t groups = (c->n_tet + 31) / 32;
-  int64_t grid = (groups + D::WARPS - 1) / D::WARPS;
-  if (grid > (int64_t)c->sms * occ) grid = (int64_t)c->sms * occ;
-  lane_trace_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(X, tr, c->n_tet);
+  const int grid = occupancy_grid(c, lane_trace_kernel<P>, D::WARPS, smem, (c->n_tet + 15) / 16);
+  lane_trace_kernel<P><<<grid, D::WARPS * 32, smem, st>>>(X, tr, c->n_tet);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("lane_trace_kernel: ") + cudaGetErrorString(e));

@@ -1,138 +1,180 @@
-"""Code generator for the lane-per-element CUDA kernels (low orders).
+"""Code generator for the lane-pair CUDA kernels (low orders, p <= 4).
 
-For small p one element fits one thread: the warp owns 32 consecutive elements,
-their coefficients live in shared memory interleaved by element
-(s[slot*33 + lane], conflict-free), and every thread runs the SAME straight-line
-program on its own element — the paper's own implementation strategy
-("template meta-programming, where the compiler can generate optimized code for
-all elements up to an a priori chosen maximal polynomial order")
-carried over to SIMT: coefficients are compile-time constants (constant bank,
-warp-uniform), operands come from conflict-free shared memory or registers.
+A warp owns 16 consecutive elements; each element is handled by a PAIR of
+lanes (half h = lane>>4) that execute the same instruction stream on
+different data, so there is no divergence:
+  * curl: for each direction d the two halves sweep the two source components
+    that ∂_d acts on: ∂x: (Ŷz → -ĉy | Ŷy → +ĉz), ∂y: (Ŷz → +ĉx | Ŷx → -ĉz),
+    ∂z: (Ŷy → -ĉx | Ŷx → +ĉy)  — same relation table, per-lane operand pointers;
+  * traces: half h computes the tangential component a_h = Ŷ·t̂_h on each face;
+  * lift: half 0 lifts B = sf D₁ (+ upwind), half 1 lifts A = -sf D₂ (+ upwind);
+  * update and X traces: halves split the modes / the tangential components.
+Shared memory is element-major, s[e*SE + slot] with an odd SE (conflict-free for 16 lanes).
+Coefficients live in one __constant__ table per order (deduplicated) so every
+DFMA takes its coefficient straight from the constant bank (warp-uniform).
 
-Emitted per order p (header lane_p{p}.cuh):
-  lane_curl_p{p}(sY, sA)        sA[m][β] = (curl̂ Ŷ)_{m,β}  (recurrence sweeps, pull form)
-  lane_trace_p{p}_f{f}(sY, t)   t[k][γ]  = Σ_α Tr_f[α,γ] (Ŷ·t̂_k)_α
-  lane_lift_p{p}_f{f}(q, sA)    sA[m][β] += Σ_γ Tr_f[β,γ]‖ψ_γ‖²/‖φ_β‖² q[m][γ]
+This is the SIMT form of the paper's "template meta-programming" straight-line
+code.  Emitted per order p (header lane_p{p}.cuh):
+  lane_sweep_p{p}_d{d}(src, dst, sgn)      dst[β] += sgn Σ b u_γ   (pull-form sweep)
+  lane_trace_p{p}_f{f}(a, sub, out, os)     out[γ·os] = Σ_α Tr_f[α,γ] (a[α] - sub[α])
+  lane_lift_p{p}_f{f}(q_0..q_NF-1, o)       o[β] += Σ_γ Tr_f[β,γ]‖ψ_γ‖²/‖φ_β‖² q_γ  (face 0 also o0 -= …)
 """
 from __future__ import annotations
 
 import os
 
 from . import plan
+from . import relations as R
 
-STRIDE = 33
-
-
-def _lit(x: float) -> str:
-    return float(x).hex()
+S = 1    # slot stride (doubles): element-major layout, slots contiguous per element
 
 
-def _fma_chain(terms, init=None):
-    """C expression of Σ coef*val as an fma chain; terms: [(coef_float, expr)]."""
-    acc = init
+class ConstTable:
+    def __init__(self, p):
+        self.p = p
+        self.vals = []
+        self.idx = {}
+
+    def ref(self, x):
+        x = float(x)
+        if x not in self.idx:
+            self.idx[x] = len(self.vals)
+            self.vals.append(x)
+        return f"LC{self.p}[{self.idx[x]}]"
+
+    def emit(self):
+        body = ",".join(float(v).hex() for v in self.vals) or "0"
+        return f"__constant__ double LC{self.p}[{max(1, len(self.vals))}] = {{{body}}};"
+
+
+def _chain(ct, terms):
+    """fma chain Σ coef*expr (coef ±1 become add/sub)."""
+    acc = None
     for cf, ex in terms:
-        if cf == 1.0 and acc is None:
-            acc = ex
-            continue
+        cf = float(cf)
         if acc is None:
-            acc = f"({_lit(cf)} * {ex})"
+            acc = ex if cf == 1.0 else (f"(-{ex})" if cf == -1.0 else f"({ct.ref(cf)} * {ex})")
         elif cf == 1.0:
             acc = f"({acc} + {ex})"
         elif cf == -1.0:
             acc = f"({acc} - {ex})"
         else:
-            acc = f"fma({_lit(cf)}, {ex}, {acc})"
+            acc = f"fma({ct.ref(cf)}, {ex}, {acc})"
     return acc if acc is not None else "0.0"
 
 
-def gen_curl(p):
-    rows, ACC = plan.curl_program(p)
-    N = plan.n_modes(p)
-    out = [f"__device__ __forceinline__ void lane_curl_p{p}(const double *__restrict__ sY, double *__restrict__ sA) {{"]
-    # slots < 3N are input loads; 3N..9N are u temporaries (registers); >= ACC outputs
-    loaded = set()
-    lines = []
-    # order rows by level so dependencies come first (levels are ASAP)
-    for dst, terms, lv in sorted(rows, key=lambda r: r[2]):
-        exprs = []
-        for s, cf in terms:
-            if s < 3 * N:
-                if s not in loaded:
-                    lines.append(f"  const double y{s} = sY[{s * STRIDE}];")
-                    loaded.add(s)
-                exprs.append((float(cf), f"y{s}"))
-            else:
-                exprs.append((float(cf), f"u{s}"))
-        e = _fma_chain(exprs)
-        if dst >= ACC:
-            lines.append(f"  sA[{(dst - ACC) * STRIDE}] = {e};")
+def gen_sweep(p, d, ct):
+    """One directional sweep (pull form) on the source component at `src`,
+    accumulating sgn*(pure terms) into `dst` (both element-interleaved, stride S)."""
+    rels, _ = plan.load(p)
+    rel = rels[d]
+    idx = R.tet_indices(p)
+    pos = {a: q for q, a in enumerate(idx)}
+    incoming = {g: [] for g in rel}
+    for g, terms in rel.items():
+        for (t, dv), coef in terms.items():
+            if dv:
+                incoming[t].append((g, coef))
+    order = sorted(rel, key=R.proc_key, reverse=True)
+    out = [f"__device__ __noinline__ void lane_sweep_p{p}_d{d}(const double *__restrict__ src, double *__restrict__ dst, double sgn) {{"]
+    uname = {}
+    acc = {}
+    for g in order:
+        v = f"src[{pos[g] * S}]"
+        if incoming[g]:
+            terms = [(1.0, v)] + [(float(a), uname[g2]) for g2, a in incoming[g]]
+            out.append(f"  const double u{pos[g]} = {_chain(ct, terms)};")
+            uname[g] = f"u{pos[g]}"
         else:
-            lines.append(f"  const double u{dst} = {e};")
-    out += lines
+            out.append(f"  const double u{pos[g]} = {v};")
+            uname[g] = f"u{pos[g]}"
+        for (t, dv), coef in rel[g].items():
+            if not dv:
+                acc.setdefault(pos[t], []).append((float(coef), uname[g]))
+    # outputs at the end (the compiler schedules the FMAs; live set ~N values at p<=4)
+    for b in sorted(acc):
+        out.append(f"  dst[{b * S}] = fma(sgn, {_chain(ct, acc[b])}, dst[{b * S}]);")
     out.append("}")
     return "\n".join(out)
 
 
-TANG = {0: ("(y{n}_{a} - y0_{a})", "(y{n2}_{a} - y0_{a})"), 1: ("y1_{a}", "y2_{a}"), 2: ("y0_{a}", "y2_{a}"),
-        3: ("y0_{a}", "y1_{a}")}
-
-
-def gen_trace(p, f):
-    prog_rows = plan.trace_tables(p)[f]
+def gen_trace(p, f, ct):
     _, T = plan.load(p)
     N, NF = plan.n_modes(p), plan.n_face_modes(p)
-    comps = {0: (0, 1, 2), 1: (1, 2), 2: (0, 2), 3: (0, 1)}[f]
-    out = [f"__device__ __forceinline__ void lane_trace_p{p}_f{f}(const double *__restrict__ sY, double (&t)[2][{NF}]) {{"]
-    out.append(f"#pragma unroll\n  for (int g = 0; g < {NF}; ++g) {{ t[0][g] = 0.0; t[1][g] = 0.0; }}")
-    for a in range(N):
-        nz = [(g, float(T[f][a][g])) for g in range(NF) if T[f][a][g] != 0]
+    sub = f == 0
+    sig = "const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ out, int os" if sub else \
+          "const double *__restrict__ a, double *__restrict__ out, int os"
+    out = [f"__device__ __noinline__ void lane_trace_p{p}_f{f}({sig}) {{"]
+    acc = {g: [] for g in range(NF)}
+    lines = []
+    for al in range(N):
+        nz = [(g, T[f][al][g]) for g in range(NF) if T[f][al][g] != 0]
         if not nz:
             continue
-        out.append("  {")
-        for c in comps:
-            out.append(f"    const double y{c} = sY[{(c * N + a) * STRIDE}];")
-        if f == 0:
-            out.append("    const double a1 = y1 - y0, a2 = y2 - y0;")
-        elif f == 1:
-            out.append("    const double a1 = y1, a2 = y2;")
-        elif f == 2:
-            out.append("    const double a1 = y0, a2 = y2;")
+        if sub:
+            lines.append(f"  const double a{al} = a[{al * S}] - b[{al * S}];")
         else:
-            out.append("    const double a1 = y0, a2 = y1;")
-        for g, cf in nz:
-            if cf == 1.0:
-                out.append(f"    t[0][{g}] += a1; t[1][{g}] += a2;")
-            elif cf == -1.0:
-                out.append(f"    t[0][{g}] -= a1; t[1][{g}] -= a2;")
-            else:
-                out.append(f"    t[0][{g}] = fma({_lit(cf)}, a1, t[0][{g}]); t[1][{g}] = fma({_lit(cf)}, a2, t[1][{g}]);")
+            lines.append(f"  const double a{al} = a[{al * S}];")
+        for g, c in nz:
+            acc[g].append((float(c), f"a{al}"))
+    out += lines
+    for g in range(NF):
+        out.append(f"  out[{g} * os] = {_chain(ct, acc[g])};")
+    out.append("}")
+    return "\n".join(out)
+
+
+def gen_lift(p, f, ct):
+    """o[β] += L_f(q)[β].  Face 0 (t̂1 = (-1,1,0), t̂2 = (-1,0,1)) also subtracts
+    L from component 0, which both halves share: the two halves take turns."""
+    _, T = plan.load(p)
+    n3, n2 = plan.norms3(p), plan.norms2(p)
+    N, NF = plan.n_modes(p), plan.n_face_modes(p)
+    qargs = ", ".join(f"double q{g}" for g in range(NF))
+    if f == 0:
+        out = [f"__device__ __noinline__ void lane_lift_p{p}_f0({qargs}, double *__restrict__ o, double *__restrict__ o0, int h) {{"]
+    else:
+        out = [f"__device__ __noinline__ void lane_lift_p{p}_f{f}({qargs}, double *__restrict__ o) {{"]
+    rows = []
+    for b in range(N):
+        terms = [(float(T[f][b][g] * n2[g] / n3[b]), f"q{g}") for g in range(NF) if T[f][b][g] != 0]
+        if terms:
+            rows.append(b)
+            out.append(f"  const double L{b} = {_chain(ct, terms)};")
+            out.append(f"  o[{b * S}] += L{b};")
+    if f == 0:
+        out.append("  __syncwarp();")
+        out.append("  if (h == 0) {")
+        out += [f"    o0[{b * S}] -= L{b};" for b in rows]
+        out.append("  }")
+        out.append("  __syncwarp();")
+        out.append("  if (h == 1) {")
+        out += [f"    o0[{b * S}] -= L{b};" for b in rows]
         out.append("  }")
     out.append("}")
     return "\n".join(out)
 
 
-def gen_lift(p, f):
-    _, T = plan.load(p)
-    n3, n2 = plan.norms3(p), plan.norms2(p)
-    N, NF = plan.n_modes(p), plan.n_face_modes(p)
-    out = [f"__device__ __forceinline__ void lane_lift_p{p}_f{f}(const double (&q)[3][{NF}], double *__restrict__ sA) {{"]
-    for b in range(N):
-        terms = [(float(T[f][b][g] * n2[g] / n3[b]), g) for g in range(NF) if T[f][b][g] != 0]
-        if not terms:
-            continue
-        for m in range(3):
-            e = _fma_chain([(cf, f"q[{m}][{g}]") for cf, g in terms])
-            out.append(f"  sA[{(m * N + b) * STRIDE}] += {e};")
-    out.append("}")
-    return "\n".join(out)
+def gen_wrappers(p):
+    NF = plan.n_face_modes(p)
+    qa = ", ".join(f"q[{g}]" for g in range(NF))
+    return "\n".join([
+        f"__device__ __forceinline__ void lane_lift_p{p}(int f, const double (&q)[{NF}], double *o, double *o0, int h) {{",
+        f"  if (f == 0) lane_lift_p{p}_f0({qa}, o, o0, h);",
+        f"  else if (f == 1) lane_lift_p{p}_f1({qa}, o);",
+        f"  else if (f == 2) lane_lift_p{p}_f2({qa}, o);",
+        f"  else lane_lift_p{p}_f3({qa}, o);",
+        "}"])
 
 
 def emit(p, path):
-    parts = [f"// GENERATED by paper_1104_4208_b200/gen/lanegen.py (p={p}) — do not edit.",
-             f"#pragma once", gen_curl(p)]
+    ct = ConstTable(p)
+    body = [gen_sweep(p, d, ct) for d in range(3)]
     for f in range(4):
-        parts.append(gen_trace(p, f))
-        parts.append(gen_lift(p, f))
+        body.append(gen_trace(p, f, ct))
+        body.append(gen_lift(p, f, ct))
+    parts = [f"// GENERATED by paper_1104_4208_b200/gen/lanegen.py (p={p}) — do not edit.", "#pragma once",
+             ct.emit()] + body + [gen_wrappers(p)]
     with open(path, "w") as fh:
         fh.write("\n\n".join(parts) + "\n")
 
