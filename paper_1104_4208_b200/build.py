@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgm.so")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
+LANE_PMAX = 6   # lane-pair kernels up to this order (must match kLanePmax in dgm_internal.h)
 
 
 def _stale(target, deps):
@@ -38,11 +39,11 @@ def build(force=False, verbose=False):
     lanedir = os.path.join(CSRC, "lane")
     os.makedirs(lanedir, exist_ok=True)
     from .gen import lanegen
-    if force or _stale(os.path.join(lanedir, "lane_p4.cuh"), [os.path.join(HERE, "gen", "lanegen.py"), inc]):
-        lanegen.emit_all(lanedir, 4)
+    if force or _stale(os.path.join(lanedir, f"lane_p{LANE_PMAX}.cuh"), [os.path.join(HERE, "gen", "lanegen.py"), inc]):
+        lanegen.emit_all(lanedir, LANE_PMAX)
     srcs = [os.path.join(CSRC, f) for f in ("dgm_host.cpp", "dgm_kernels.cu", "dgm_lane.cu")]
     deps = srcs + [inc, os.path.join(CSRC, "dgm_internal.h"), os.path.join(HERE, "..", "include", "dgm.h"),
-                   os.path.join(lanedir, "lane_p4.cuh")]
+                   os.path.join(lanedir, f"lane_p{LANE_PMAX}.cuh")]
     if not force and not _stale(LIB, deps):
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -80,7 +80,6 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_nbrf);
   cudaFree(c->d_fmet);
   cudaFree(c->d_blob);
-  cudaFree(c->d_trX);
   for (int i = 0; i < 4; ++i) cudaFree(c->d_tr[i]);
   cudaFree(c->d_partial);
   cudaFree(c->d_E);
@@ -253,11 +252,13 @@ dgm_status upload_impl(dgm_ctx *c) {
   if (c->flux == DGM_FLUX_UPWIND) {
     CUDA_TRY(c, cudaMalloc(&c->d_fmet, sizeof(double) * 12 * n));
     CUDA_TRY(c, cudaMemcpy(c->d_fmet, c->h_fmet.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMalloc(&c->d_trX, sizeof(double) * n * 8 * c->NF));
   }
-  if (c->p <= dgm::kLanePmax)
-    for (int i = 0; i < 4; ++i)   // groups of 16 elements interleaved: round up
-      CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * ((n + 15) / 16 * 16) * 8 * c->NF));
+  // trace buffers TE0, TE1, TH0, TH1 (the second of each only for upwind); the lane
+  // path interleaves groups of 16 elements, so round up
+  for (int i = 0; i < 4; ++i) {
+    if ((i == 1 || i == 3) && c->flux != DGM_FLUX_UPWIND) continue;
+    CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * ((n + 15) / 16 * 16) * 8 * c->NF));
+  }
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
   for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);
@@ -321,19 +322,11 @@ dgm_status dgm_apply_curl(dgm_ctx *c, const double *E, const double *H, double *
   if (!c || !E || !H) return dgm::set_err(c, DGM_EINVAL, "null pointer");
   cudaStream_t st = (cudaStream_t)stream;
   c->launches = 0;
-  if (c->p <= dgm::kLanePmax) {
-    dgm_status s = DGM_OK;
-    if (dE) s = dgm::launch_lane_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
-    if (s == DGM_OK && dH)
-      s = dgm::launch_lane_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
-    return s;
-  }
-  if (dE) {
-    dgm_status s = dgm::launch_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, st);
-    if (s != DGM_OK) return s;
-  }
-  if (dH) return dgm::launch_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 0, dgm::OUT_WRITE, st);
-  return DGM_OK;
+  dgm_status s = DGM_OK;
+  if (dE) s = dgm::launch_tb_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
+  if (s == DGM_OK && dH)
+    s = dgm::launch_tb_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 0, dgm::OUT_WRITE, nullptr, nullptr, nullptr, st);
+  return s;
 }
 
 dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *dE, double *dH, int accumulate,
@@ -342,30 +335,14 @@ dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *
   cudaStream_t st = (cudaStream_t)stream;
   int om = accumulate ? dgm::OUT_ACCUM : dgm::OUT_WRITE;
   c->launches = 0;
-  if (c->p <= dgm::kLanePmax) {
-    double *TE = c->d_tr[0], *TH = c->d_tr[2];
-    dgm_status s = dgm::launch_lane_traces(c, E, TE, st);
-    if (s == DGM_OK) s = dgm::launch_lane_traces(c, H, TH, st);
-    if (s == DGM_OK && dE) s = dgm::launch_lane_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, TH, TE, nullptr, st);
-    if (s == DGM_OK && dH) s = dgm::launch_lane_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, TE, TH, nullptr, st);
-    return s;
-  }
-  if (dE) {
-    if (c->flux == DGM_FLUX_UPWIND) {
-      dgm_status s = dgm::launch_traces(c, E, st);
-      if (s != DGM_OK) return s;
-    }
-    dgm_status s = dgm::launch_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, st);
-    if (s != DGM_OK) return s;
-  }
-  if (dH) {
-    if (c->flux == DGM_FLUX_UPWIND) {
-      dgm_status s = dgm::launch_traces(c, H, st);
-      if (s != DGM_OK) return s;
-    }
-    return dgm::launch_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, st);
-  }
-  return DGM_OK;
+  // traces of both fields, then the face parts: the E equation reads H's traces
+  // (and, upwind, E's own), the H equation the other way round
+  double *TE = c->d_tr[0], *TH = c->d_tr[2];
+  dgm_status s = dgm::launch_tb_traces(c, E, TE, st);
+  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st);
+  if (s == DGM_OK && dE) s = dgm::launch_tb_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, TH, TE, nullptr, st);
+  if (s == DGM_OK && dH) s = dgm::launch_tb_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, TE, TH, nullptr, st);
+  return s;
 }
 
 dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, void *stream) {
@@ -373,32 +350,25 @@ dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps,
   cudaStream_t st = (cudaStream_t)stream;
   c->launches = 0;
   if (nsteps == 0) return DGM_OK;
-  if (c->p <= dgm::kLanePmax) {
-    // traces of the field each stage reads from its neighbours are produced by the
-    // stage that updated it; recomputed at entry so that resume is exact.
-    const bool up = c->flux == DGM_FLUX_UPWIND;
-    int ce = 0, ch = 0;
-    dgm_status r = dgm::launch_lane_traces(c, E, c->d_tr[0], st);
-    if (r == DGM_OK && up) r = dgm::launch_lane_traces(c, H, c->d_tr[2], st);
-    for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
-      double *TE = c->d_tr[ce], *THr = c->d_tr[2 + ch], *THw = c->d_tr[2 + (up ? 1 - ch : ch)];
-      r = dgm::launch_lane_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
-      if (up) ch = 1 - ch;
-      if (r != DGM_OK) break;
-      double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
-      r = dgm::launch_lane_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
-      if (up) ce = 1 - ce;
-    }
-    return r;
+  // Each stage reads the traces of the field it does not update (own and
+  // neighbours) from the buffer written by the stage that last updated that
+  // field, and writes the traces of the field it updates.  They are recomputed
+  // at entry so that resuming from saved (E, H) is exact.  Upwind also reads
+  // the old traces of the updated field, so those buffers ping-pong.
+  const bool up = c->flux == DGM_FLUX_UPWIND;
+  int ce = 0, ch = 0;
+  dgm_status r = dgm::launch_tb_traces(c, E, c->d_tr[0], st);
+  if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st);
+  for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
+    double *TE = c->d_tr[ce], *THr = c->d_tr[2 + ch], *THw = c->d_tr[2 + (up ? 1 - ch : ch)];
+    r = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
+    if (up) ch = 1 - ch;
+    if (r != DGM_OK) break;
+    double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
+    r = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
+    if (up) ce = 1 - ce;
   }
-  for (int64_t s = 0; s < nsteps; ++s) {
-    dgm_status r;
-    if (c->flux == DGM_FLUX_UPWIND && (r = dgm::launch_traces(c, H, st)) != DGM_OK) return r;
-    if ((r = dgm::launch_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, st)) != DGM_OK) return r;
-    if (c->flux == DGM_FLUX_UPWIND && (r = dgm::launch_traces(c, E, st)) != DGM_OK) return r;
-    if ((r = dgm::launch_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, st)) != DGM_OK) return r;
-  }
-  return DGM_OK;
+  return r;
 }
 
 dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t nsteps, void *stream) {

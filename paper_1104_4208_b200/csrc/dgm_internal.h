@@ -58,7 +58,7 @@ struct StageArgs {
   const double *Y;       // other field (curl and central-flux source)
   double *X;             // updated field (OUT_UPDATE)
   double *dX;            // derivative output (OUT_WRITE / OUT_ACCUM)
-  const double *trX;     // upwind: tangential traces of the updated field [n][4][2][NF]
+  const double *trX;     // upwind: tangential traces of the updated field (trace-buffer layout)
   const Geo *geo;
   const int32_t *nbr;    // [n][4], -1 PEC
   const int8_t *nbrf;    // [n][4], -1 PEC
@@ -85,7 +85,6 @@ struct dgm_ctx {
   double *d_fmet = nullptr;
   void *d_blob = nullptr;
   dgm::DevProgs progs{};
-  double *d_trX = nullptr;     // upwind trace buffer (warp path)
   double *d_tr[4] = {nullptr, nullptr, nullptr, nullptr};  // lane path: TE0, TE1, TH0, TH1
   double *d_partial = nullptr; // energy partial sums
   int64_t n_partial = 0;
@@ -97,13 +96,15 @@ struct dgm_ctx {
 namespace dgm {
 dgm_status set_err(dgm_ctx *c, dgm_status s, const std::string &msg);
 // kernels (dgm_kernels.cu)
-dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt,
-                        int do_curl, int do_flux, int out_mode, cudaStream_t st);
-dgm_status launch_traces(dgm_ctx *c, const double *X, cudaStream_t st);
+// trace-buffer stage scheme for all orders (lane-pair kernels p <= kLanePmax, warp kernels above)
+dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
+                           int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
+                           cudaStream_t st);
+dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
 int workspace_doubles(int p);
 // lane-per-element path (dgm_lane.cu), p <= kLanePmax
-constexpr int kLanePmax = 4;
+constexpr int kLanePmax = 6;
 dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
                              int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
                              cudaStream_t st);

@@ -32,6 +32,19 @@ struct Dim {
   static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
 };
 
+// warp path with trace buffers: slots [0,9N) sweep (Ŷ then u), acc at 9N, A/B at 12N
+template <int P>
+struct Dim2 {
+  static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
+  static constexpr int NF = (P + 1) * (P + 2) / 2;
+  static constexpr int LD = (N + 3) & ~3;
+  static constexpr int ACC = 9 * N;   // must match gen/plan.py
+  static constexpr int SAB = 12 * N;
+  static constexpr int WS = 12 * N + 2 * NF;
+  static constexpr int WARPS_RAW = (200 * 1024) / (WS * 8);
+  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
+};
+
 // Reference face tangents t̂1 = v̂b - v̂a, t̂2 = v̂c - v̂a (reading G9).
 __constant__ double kT1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
 __constant__ double kT2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
@@ -136,26 +149,55 @@ __device__ __forceinline__ void load_elem(const double *__restrict__ F, int64_t 
   }
 }
 
-template <int P>
-__global__ void __launch_bounds__(Dim<P>::WARPS * 32) stage_kernel(StageArgs a, DevProgs pr) {
-  using D = Dim<P>;
+// lift of the two face fields A, B (face f) into the accumulator:
+// acc[m][β] += t̂1_m Σ_γ L_f[β,γ] A_γ + t̂2_m Σ_γ L_f[β,γ] B_γ
+__device__ __forceinline__ void run_lift2(const DevProg &p, const double *AB, int N, int NF, double *acc, int f,
+                                          int lane) {
+  const double a0 = kT1[f][0], a1 = kT1[f][1], a2 = kT1[f][2];
+  const double b0 = kT2[f][0], b1 = kT2[f][1], b2 = kT2[f][2];
+  for (int ps = 0; ps < p.npass; ++ps) {
+    const int row = ps * 32 + lane;
+    const unsigned b = __ldg(p.dst + row);
+    if (b != 0xFFFFu) {
+      const int c = __ldg(p.cnt + row);
+      const int o = __ldg(p.off + ps) * 32 + lane;
+      double la = 0.0, lb = 0.0;
+#pragma unroll 4
+      for (int t = 0; t < c; ++t) {
+        const int g = __ldg(p.src + o + 32 * t);
+        const double cf = __ldg(p.coef + o + 32 * t);
+        la = fma(cf, AB[g], la);
+        lb = fma(cf, AB[NF + g], lb);
+      }
+      acc[b] += a0 * la + b0 * lb;
+      acc[N + b] += a1 * la + b1 * lb;
+      acc[2 * N + b] += a2 * la + b2 * lb;
+    }
+  }
+}
+
+// Warp-per-element stage kernel for p > kLanePmax (trace-buffer scheme).  One
+// warp owns one element at a time.  Own and neighbour traces of Ŷ are read from
+// the trace buffer tr[e][f][k][γ] written by the stage that last updated Ŷ; the
+// lift acts on the two face fields A = -sf D₂ (+ upwind), B = sf D₁ (+ upwind),
+// acc_m += t̂1_m L_f(A) + t̂2_m L_f(B); after the update the warp writes the
+// traces of the updated field for the next stage.
+template <int P, bool UP>
+__global__ void __launch_bounds__(Dim2<P>::WARPS * 32)
+    stage2_kernel(StageArgs a, DevProgs pr, const double *__restrict__ trY, double *__restrict__ trOut) {
+  using D = Dim2<P>;
   constexpr int N = D::N, NF = D::NF, LD = D::LD;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *s = smem + warp * D::WS;
-  double *sY = s;
   double *sACC = s + D::ACC;
-  double *sTO = s + D::FLUX_BASE;   // own traces [4][2][NF]
-  double *sNB = sTO + 8 * NF;       // neighbour volume staging [3][N]
-  double *sTN = sNB + 3 * N;        // neighbour traces [2][NF]
-  double *sQ = sTN + 2 * NF;        // face vectors [3][NF]
-  const int64_t cstride = a.n_tet * LD;
+  double *sAB = s + D::SAB;
+  const int64_t cs = a.n_tet * LD;
   const bool stageE = a.stage == STAGE_E;
-  const double mirrorY = stageE ? 1.0 : -1.0;   // PEC: H⁺=H⁻ (Y=H), E⁺=-E⁻ (Y=E)
-  const double mirrorX = stageE ? -1.0 : 1.0;
-
+  const bool upd = a.out_mode == OUT_UPDATE;
+  const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
   for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < a.n_tet; e += (int64_t)gridDim.x * D::WARPS) {
-    load_elem<LD, N>(a.Y, e, cstride, sY, lane);
+    load_elem<LD, N>(a.Y, e, cs, s, lane);
     __syncwarp();
     if (a.do_curl) {
       run_assign(pr.curl, s, lane);
@@ -163,24 +205,17 @@ __global__ void __launch_bounds__(Dim<P>::WARPS * 32) stage_kernel(StageArgs a, 
       for (int i = lane; i < 3 * N; i += 32) sACC[i] = 0.0;
     }
     __syncwarp();
+    // Ŷ is dead (traces come from the buffer): stage X in its slots
+    if (upd) load_elem<LD, N>(a.X, e, cs, s, lane);
     const Geo g = a.geo[e];
     if (a.do_flux) {
-      for (int f = 0; f < 4; ++f) run_trace(pr, f, sY, N, NF, sTO + 2 * NF * f, lane);
-      __syncwarp();
       const double sgn = g.detF > 0 ? 1.0 : -1.0;
       for (int f = 0; f < 4; ++f) {
         const int nb = a.nbr[4 * e + f];
         const int gf = a.nbrf[4 * e + f];
-        if (nb >= 0) {
-          load_elem<LD, N>(a.Y, nb, cstride, sNB, lane);
-          __syncwarp();
-          run_trace(pr, gf, sNB, N, NF, sTN, lane);
-          __syncwarp();
-        }
         double w = 0.5, k = 0.0;
-        double Zm = g.Z, Zp = Zm;
-        if (a.upwind) {
-          if (nb >= 0) Zp = a.geo[nb].Z;
+        if (UP) {
+          const double Zm = g.Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
           if (stageE) {
             w = Zp / (Zm + Zp);
             k = 1.0 / (Zm + Zp);
@@ -191,46 +226,40 @@ __global__ void __launch_bounds__(Dim<P>::WARPS * 32) stage_kernel(StageArgs a, 
           }
         }
         const double sf = (f & 1) ? -1.0 : 1.0;
-        const double *to = sTO + 2 * NF * f;
+        const double *to = trY + (e * 4 + f) * 2 * NF;
+        const double *tn = nb >= 0 ? trY + ((int64_t)nb * 4 + gf) * 2 * NF : nullptr;
         for (int gm = lane; gm < NF; gm += 32) {
-          const double yo1 = to[gm], yo2 = to[NF + gm];
-          const double yn1 = nb >= 0 ? sTN[gm] : mirrorY * yo1;
-          const double yn2 = nb >= 0 ? sTN[NF + gm] : mirrorY * yo2;
-          const double d1 = w * (yn1 - yo1), d2 = w * (yn2 - yo2);
-          double q0 = sf * (d1 * kT2[f][0] - d2 * kT1[f][0]);
-          double q1 = sf * (d1 * kT2[f][1] - d2 * kT1[f][1]);
-          double q2 = sf * (d1 * kT2[f][2] - d2 * kT1[f][2]);
-          if (a.upwind) {
-            const double *tx = a.trX + ((e * 4 + f) * 2) * NF;
-            const double xo1 = tx[gm], xo2 = tx[NF + gm];
+          const double o1 = __ldg(to + gm), o2 = __ldg(to + NF + gm);
+          const double n1 = nb >= 0 ? __ldg(tn + gm) : mirrorY * o1;
+          const double n2 = nb >= 0 ? __ldg(tn + NF + gm) : mirrorY * o2;
+          double A = -sf * w * (n2 - o2), B = sf * w * (n1 - o1);
+          if (UP) {
+            const double *xo = a.trX + (e * 4 + f) * 2 * NF;
+            const double xo1 = __ldg(xo + gm), xo2 = __ldg(xo + NF + gm);
             double xn1, xn2;
             if (nb >= 0) {
-              const double *tn = a.trX + (((int64_t)nb * 4 + gf) * 2) * NF;
-              xn1 = tn[gm];
-              xn2 = tn[NF + gm];
+              const double *xn = a.trX + ((int64_t)nb * 4 + gf) * 2 * NF;
+              xn1 = __ldg(xn + gm);
+              xn2 = __ldg(xn + NF + gm);
             } else {
               xn1 = mirrorX * xo1;
               xn2 = mirrorX * xo2;
             }
             const double j1 = k * (xn1 - xo1), j2 = k * (xn2 - xo2);
             const double *M = a.fmet + 12 * e + 3 * f;
-            const double p1 = j1 * M[0] + j2 * M[1];
-            const double p2 = j1 * M[1] + j2 * M[2];
             const double ps = (stageE ? 1.0 : -1.0) * sgn;
-            q0 += ps * (p1 * kT1[f][0] + p2 * kT2[f][0]);
-            q1 += ps * (p1 * kT1[f][1] + p2 * kT2[f][1]);
-            q2 += ps * (p1 * kT1[f][2] + p2 * kT2[f][2]);
+            A += ps * (j1 * M[0] + j2 * M[1]);
+            B += ps * (j1 * M[1] + j2 * M[2]);
           }
-          sQ[gm] = q0;
-          sQ[NF + gm] = q1;
-          sQ[2 * NF + gm] = q2;
+          sAB[gm] = A;
+          sAB[NF + gm] = B;
         }
         __syncwarp();
-        run_lift(pr.lift[f], sQ, N, NF, sACC, lane);
+        run_lift2(pr.lift[f], sAB, N, NF, sACC, f, lane);
         __syncwarp();
       }
     }
-    // S2 + S6: inverse mass with geometry, then update or write
+    // S2 + S6: inverse mass with geometry, then update (X staged in slots [0,3N)) or write
     const double cm = stageE ? g.inv_eps : -g.inv_mu;
     for (int b = lane; b < N; b += 32) {
       const double v0 = sACC[b], v1 = sACC[N + b], v2 = sACC[2 * N + b];
@@ -238,41 +267,46 @@ __global__ void __launch_bounds__(Dim<P>::WARPS * 32) stage_kernel(StageArgs a, 
       const double x1 = cm * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
       const double x2 = cm * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
       const int64_t o = e * LD + b;
-      if (a.out_mode == OUT_UPDATE) {
-        a.X[o] += a.dt * x0;
-        a.X[cstride + o] += a.dt * x1;
-        a.X[2 * cstride + o] += a.dt * x2;
+      if (upd) {
+        const double y0 = s[b] + a.dt * x0, y1 = s[N + b] + a.dt * x1, y2 = s[2 * N + b] + a.dt * x2;
+        s[b] = y0;
+        s[N + b] = y1;
+        s[2 * N + b] = y2;
+        a.X[o] = y0;
+        a.X[cs + o] = y1;
+        a.X[2 * cs + o] = y2;
       } else if (a.out_mode == OUT_WRITE) {
         a.dX[o] = x0;
-        a.dX[cstride + o] = x1;
-        a.dX[2 * cstride + o] = x2;
+        a.dX[cs + o] = x1;
+        a.dX[2 * cs + o] = x2;
       } else {
         a.dX[o] += x0;
-        a.dX[cstride + o] += x1;
-        a.dX[2 * cstride + o] += x2;
+        a.dX[cs + o] += x1;
+        a.dX[2 * cs + o] += x2;
       }
+    }
+    __syncwarp();
+    if (upd && trOut) {
+      for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, trOut + (e * 4 + f) * 2 * NF, lane);
     }
     __syncwarp();
   }
 }
 
-// Upwind: tangential traces of the updated field for all elements -> trX[e][f][k][γ]
+// tangential traces of a field for all elements -> tr[e][f][k][γ] (warp path layout)
 template <int P>
-__global__ void __launch_bounds__(Dim<P>::WARPS * 32) trace_kernel(const double *__restrict__ X, double *trX,
-                                                                    int64_t n_tet, DevProgs pr) {
-  using D = Dim<P>;
+__global__ void __launch_bounds__(Dim2<P>::WARPS * 32) trace2_kernel(const double *__restrict__ X, double *tr,
+                                                                      int64_t n_tet, DevProgs pr) {
+  using D = Dim2<P>;
   constexpr int N = D::N, NF = D::NF, LD = D::LD;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double *s = smem + warp * D::WS;
-  double *out = s + 3 * N;
-  const int64_t cstride = n_tet * LD;
+  const int64_t cs = n_tet * LD;
   for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < n_tet; e += (int64_t)gridDim.x * D::WARPS) {
-    load_elem<LD, N>(X, e, cstride, s, lane);
+    load_elem<LD, N>(X, e, cs, s, lane);
     __syncwarp();
-    for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, out + 2 * NF * f, lane);
-    __syncwarp();
-    for (int i = lane; i < 8 * NF; i += 32) trX[e * 8 * NF + i] = out[i];
+    for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, tr + (e * 4 + f) * 2 * NF, lane);
     __syncwarp();
   }
 }
@@ -334,48 +368,55 @@ __global__ void sum_kernel(const double *partial, int n, double *out) {
 
 // ---------------------------------------------------------------------------
 template <int P>
-static dgm_status launch_stage_p(dgm_ctx *c, const StageArgs &a, cudaStream_t st) {
-  using D = Dim<P>;
+static dgm_status launch_stage2_p(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
+  using D = Dim2<P>;
   const size_t smem = sizeof(double) * D::WS * D::WARPS;
-  static bool attr_set = false;
-  static int occ = 0;
-  if (!attr_set) {
-    cudaFuncSetAttribute(stage_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<P>, D::WARPS * 32, smem);
+  auto go = [&](auto kernel) {
+    int occ = 0;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, D::WARPS * 32, smem);
     if (occ < 1) occ = 1;
-    attr_set = true;
-  }
-  int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
-  int64_t grid = (int64_t)c->sms * occ;
-  if (grid > need) grid = need;
-  stage_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(a, c->progs);
+    int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
+    int64_t grid = (int64_t)c->sms * occ;
+    if (grid > need) grid = need;
+    kernel<<<(unsigned)grid, D::WARPS * 32, smem, st>>>(a, c->progs, trY, trOut);
+  };
+  if (a.upwind) go(stage2_kernel<P, true>);
+  else go(stage2_kernel<P, false>);
   c->launches++;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("stage_kernel: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("stage2_kernel: ") + cudaGetErrorString(e));
   return DGM_OK;
 }
 
 template <int P>
-static dgm_status launch_traces_p(dgm_ctx *c, const double *X, cudaStream_t st) {
-  using D = Dim<P>;
+static dgm_status launch_trace2_p(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
+  using D = Dim2<P>;
   const size_t smem = sizeof(double) * D::WS * D::WARPS;
-  static bool attr_set = false;
-  static int occ = 0;
-  if (!attr_set) {
-    cudaFuncSetAttribute(trace_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace_kernel<P>, D::WARPS * 32, smem);
-    if (occ < 1) occ = 1;
-    attr_set = true;
-  }
+  int occ = 0;
+  cudaFuncSetAttribute(trace2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace2_kernel<P>, D::WARPS * 32, smem);
+  if (occ < 1) occ = 1;
   int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
   int64_t grid = (int64_t)c->sms * occ;
   if (grid > need) grid = need;
-  trace_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(X, c->d_trX, c->n_tet, c->progs);
+  trace2_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(X, tr, c->n_tet, c->progs);
   c->launches++;
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("trace_kernel: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("trace2_kernel: ") + cudaGetErrorString(e));
   return DGM_OK;
 }
+
+#define DGM_DISPATCH_HI(p, fn, ...)      \
+  switch (p) {                           \
+    case 5: return fn<5>(__VA_ARGS__);   \
+    case 6: return fn<6>(__VA_ARGS__);   \
+    case 7: return fn<7>(__VA_ARGS__);   \
+    case 8: return fn<8>(__VA_ARGS__);   \
+    case 9: return fn<9>(__VA_ARGS__);   \
+    case 10: return fn<10>(__VA_ARGS__); \
+    default: return DGM_EORDER;          \
+  }
 
 #define DGM_DISPATCH(p, fn, ...)          \
   switch (p) {                            \
@@ -392,14 +433,17 @@ static dgm_status launch_traces_p(dgm_ctx *c, const double *X, cudaStream_t st) 
     default: return DGM_EORDER;           \
   }
 
-dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
-                        int do_flux, int out_mode, cudaStream_t st) {
+dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
+                           int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
+                           cudaStream_t st) {
   if (c->n_tet == 0) return DGM_OK;
+  if (c->p <= kLanePmax)
+    return launch_lane_stage(c, stage, Y, X, dX, dt, do_curl, do_flux, out_mode, trY, trX, trOut, st);
   StageArgs a;
   a.Y = Y;
   a.X = X;
   a.dX = dX;
-  a.trX = c->d_trX;
+  a.trX = trX;
   a.geo = c->d_geo;
   a.nbr = c->d_nbr;
   a.nbrf = c->d_nbrf;
@@ -411,12 +455,13 @@ dgm_status launch_stage(dgm_ctx *c, int stage, const double *Y, double *X, doubl
   a.do_curl = do_curl;
   a.do_flux = do_flux;
   a.out_mode = out_mode;
-  DGM_DISPATCH(c->p, launch_stage_p, c, a, st)
+  DGM_DISPATCH_HI(c->p, launch_stage2_p, c, a, trY, trOut, st)
 }
 
-dgm_status launch_traces(dgm_ctx *c, const double *X, cudaStream_t st) {
+dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
   if (c->n_tet == 0) return DGM_OK;
-  DGM_DISPATCH(c->p, launch_traces_p, c, X, st)
+  if (c->p <= kLanePmax) return launch_lane_traces(c, X, tr, st);
+  DGM_DISPATCH_HI(c->p, launch_trace2_p, c, X, tr, st)
 }
 
 template <int P>

@@ -21,6 +21,8 @@
 #include "lane/lane_p2.cuh"
 #include "lane/lane_p3.cuh"
 #include "lane/lane_p4.cuh"
+#include "lane/lane_p5.cuh"
+#include "lane/lane_p6.cuh"
 
 namespace dgm {
 
@@ -67,6 +69,8 @@ DGM_L2_OPS(1)
 DGM_L2_OPS(2)
 DGM_L2_OPS(3)
 DGM_L2_OPS(4)
+DGM_L2_OPS(5)
+DGM_L2_OPS(6)
 
 // tangential component h of face f: a_h = Y[c] (- Y[0] on face 0)
 __device__ __forceinline__ int tang_comp(int f, int h) {
@@ -408,6 +412,8 @@ dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, 
     case 2: return lane_stage_p<2>(c, a, trY, trOut, st);
     case 3: return lane_stage_p<3>(c, a, trY, trOut, st);
     case 4: return lane_stage_p<4>(c, a, trY, trOut, st);
+    case 5: return lane_stage_p<5>(c, a, trY, trOut, st);
+    case 6: return lane_stage_p<6>(c, a, trY, trOut, st);
   }
   return DGM_EORDER;
 }
@@ -419,6 +425,8 @@ dgm_status launch_lane_traces(dgm_ctx *c, const double *X, double *tr, cudaStrea
     case 2: return lane_trace_p<2>(c, X, tr, st);
     case 3: return lane_trace_p<3>(c, X, tr, st);
     case 4: return lane_trace_p<4>(c, X, tr, st);
+    case 5: return lane_trace_p<5>(c, X, tr, st);
+    case 6: return lane_trace_p<6>(c, X, tr, st);
   }
   return DGM_EORDER;
 }
