@@ -109,6 +109,17 @@ dgm_status dgm_apply_flux(dgm_ctx *ctx, const double *E, const double *H, double
  * of the field being updated. */
 dgm_status dgm_step(dgm_ctx *ctx, double *E, double *H, double dt, int64_t nsteps, void *cuda_stream);
 
+/* Flags for dgm_step_ex. */
+#define DGM_STEP_CONTINUE 1  /* E, H are the arrays of the previous dgm_step/_ex call on this
+                                context and were not modified since: reuse the face-trace
+                                buffers that call left instead of recomputing them at entry
+                                (falls back to recomputing if the pointers differ or another
+                                call invalidated the buffers). */
+
+/* dgm_step with flags (0 = identical to dgm_step). */
+dgm_status dgm_step_ex(dgm_ctx *ctx, double *E, double *H, double dt, int64_t nsteps, int flags,
+                       void *cuda_stream);
+
 /* Same as dgm_step on HOST arrays (layout as above): copies E,H host→device,
  * steps, copies back device→host, synchronises.  The context keeps the device
  * copies between calls.  Host arrays should be pinned for full copy speed. */

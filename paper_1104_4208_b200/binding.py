@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(HERE, "libdgm.so")
 DGM_OK, DGM_EINVAL, DGM_EMESH, DGM_EORDER, DGM_ECUDA, DGM_ENOMEM = range(6)
 STATUS = {0: "DGM_OK", 1: "DGM_EINVAL", 2: "DGM_EMESH", 3: "DGM_EORDER", 4: "DGM_ECUDA", 5: "DGM_ENOMEM"}
 FLUX = {"central": 0, "upwind": 1}
-EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_host",
+DGM_STEP_CONTINUE = 1
+EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
            "dgm_energy", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
 
 
@@ -55,6 +56,7 @@ def load_library(path: str = LIB_PATH):
         "dgm_apply_curl": (I32, [P, P, P, P, P, P]),
         "dgm_apply_flux": (I32, [P, P, P, P, P, I32, P]),
         "dgm_step": (I32, [P, P, P, D, I64, P]),
+        "dgm_step_ex": (I32, [P, P, P, D, I64, I32, P]),
         "dgm_step_host": (I32, [P, P, P, D, I64, P]),
         "dgm_energy": (I32, [P, P, P, P, P]),
         "dgm_tables": (I32, [P, P, P, P, P]),
@@ -162,6 +164,11 @@ class Context:
     def dgm_step(self, E, H, dt, nsteps=1, stream=None):
         self._check(self._lib.dgm_step(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
                                        float(dt), int(nsteps), _stream(stream)))
+
+    def dgm_step_ex(self, E, H, dt, nsteps=1, flags=0, stream=None):
+        """flags: DGM_STEP_CONTINUE (=1) reuses the trace buffers of the previous call on E, H."""
+        self._check(self._lib.dgm_step_ex(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
+                                          float(dt), int(nsteps), int(flags), _stream(stream)))
 
     def dgm_step_host(self, E_host, H_host, dt, nsteps=1, stream=None):
         """E_host, H_host: CPU float64 tensors [3, n_tet, ld] (pinned for speed)."""

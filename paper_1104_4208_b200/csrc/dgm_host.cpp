@@ -338,6 +338,7 @@ dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *
   // traces of both fields, then the face parts: the E equation reads H's traces
   // (and, upwind, E's own), the H equation the other way round
   double *TE = c->d_tr[0], *TH = c->d_tr[2];
+  c->tr_valid = false;   // the buffers now hold the traces of these E, H
   dgm_status s = dgm::launch_tb_traces(c, E, TE, st);
   if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st);
   if (s == DGM_OK && dE) s = dgm::launch_tb_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, TH, TE, nullptr, st);
@@ -346,6 +347,10 @@ dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *
 }
 
 dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, void *stream) {
+  return dgm_step_ex(c, E, H, dt, nsteps, 0, stream);
+}
+
+dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, int flags, void *stream) {
   if (!c || !E || !H || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
   cudaStream_t st = (cudaStream_t)stream;
   c->launches = 0;
@@ -357,8 +362,15 @@ dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps,
   // the old traces of the updated field, so those buffers ping-pong.
   const bool up = c->flux == DGM_FLUX_UPWIND;
   int ce = 0, ch = 0;
-  dgm_status r = dgm::launch_tb_traces(c, E, c->d_tr[0], st);
-  if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st);
+  dgm_status r = DGM_OK;
+  if ((flags & DGM_STEP_CONTINUE) && c->tr_valid && c->tr_E == E && c->tr_H == H) {
+    ce = c->tr_ce;
+    ch = c->tr_ch;
+  } else {
+    r = dgm::launch_tb_traces(c, E, c->d_tr[0], st);
+    if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st);
+  }
+  c->tr_valid = false;
   for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
     double *TE = c->d_tr[ce], *THr = c->d_tr[2 + ch], *THw = c->d_tr[2 + (up ? 1 - ch : ch)];
     r = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
@@ -367,6 +379,13 @@ dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps,
     double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
     r = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
     if (up) ce = 1 - ce;
+  }
+  if (r == DGM_OK) {
+    c->tr_valid = true;
+    c->tr_E = E;
+    c->tr_H = H;
+    c->tr_ce = ce;
+    c->tr_ch = ch;
   }
   return r;
 }
@@ -381,6 +400,7 @@ dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t 
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->d_E, Eh, bytes, cudaMemcpyHostToDevice, st));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_H, Hh, bytes, cudaMemcpyHostToDevice, st));
+  c->tr_valid = false;   // fresh host data
   dgm_status s = dgm_step(c, c->d_E, c->d_H, dt, nsteps, stream);
   if (s != DGM_OK) return s;
   CUDA_TRY(c, cudaMemcpyAsync(Eh, c->d_E, bytes, cudaMemcpyDeviceToHost, st));

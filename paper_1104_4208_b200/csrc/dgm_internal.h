@@ -90,6 +90,10 @@ struct dgm_ctx {
   int64_t n_partial = 0;
   double *d_E = nullptr, *d_H = nullptr;   // device copies for dgm_step_host
   int64_t launches = 0;
+  // trace-buffer state left by the last dgm_step (for DGM_STEP_CONTINUE)
+  bool tr_valid = false;
+  const double *tr_E = nullptr, *tr_H = nullptr;
+  int tr_ce = 0, tr_ch = 0;
   std::string err;
 };
 

@@ -188,3 +188,29 @@ def test_bad_inputs_fail_loudly():
         Context(m.xyz, m.tet[:, ::-1].copy(), 2)     # non-canonical vertex order
     with pytest.raises(DgmError):
         Context(m.xyz, m.tet, 2, eps=-1.0)
+
+
+@pytest.mark.parametrize("case", ["pec-central", "mixed-upwind"])
+@pytest.mark.parametrize("p", [3, 7])
+def test_step_continue_matches_single_call(case, p):
+    """DGM_STEP_CONTINUE: k calls of 1 step reusing the trace buffers give the
+    same bits as one call of k steps; after dgm_apply_flux the buffers are
+    invalidated and the call falls back to recomputing them."""
+    from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
+    periodic, flux, n = CASES[case]
+    m, rep, eps, mu = _problem(n, periodic, p, flux)
+    c = _ctx(m, rep, p, eps, mu, flux)
+    rng = np.random.default_rng(p)
+    E = rng.standard_normal((3, m.n_tet, c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N))
+    E1, H1 = c.to_device(E), c.to_device(H)
+    c.dgm_step(E1, H1, 1e-3, 6)
+    E2, H2 = c.to_device(E), c.to_device(H)
+    c.dgm_step(E2, H2, 1e-3, 1)
+    for _ in range(4):
+        c.dgm_step_ex(E2, H2, 1e-3, 1, DGM_STEP_CONTINUE)
+        assert c.dgm_last_launches() == 2
+    c.dgm_apply_flux(E2, H2, c.empty_field(), None)     # invalidates the buffers
+    c.dgm_step_ex(E2, H2, 1e-3, 1, DGM_STEP_CONTINUE)
+    assert c.dgm_last_launches() > 2
+    assert bool((E1 == E2).all()) and bool((H1 == H2).all())
