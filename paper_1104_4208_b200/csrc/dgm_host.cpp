@@ -254,10 +254,11 @@ dgm_status upload_impl(dgm_ctx *c) {
     CUDA_TRY(c, cudaMemcpy(c->d_fmet, c->h_fmet.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice));
   }
   // trace buffers TE0, TE1, TH0, TH1 (the second of each only for upwind); the lane
-  // path interleaves groups of 16 elements, so round up
+  // path interleaves groups of 16 elements, so round up, plus 16 spare elements that
+  // absorb the writes of unused slots of a partial last group
   for (int i = 0; i < 4; ++i) {
     if ((i == 1 || i == 3) && c->flux != DGM_FLUX_UPWIND) continue;
-    CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * ((n + 15) / 16 * 16) * 8 * c->NF));
+    CUDA_TRY(c, cudaMalloc(&c->d_tr[i], sizeof(double) * ((n + 15) / 16 * 16 + 16) * 8 * c->NF));
   }
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;

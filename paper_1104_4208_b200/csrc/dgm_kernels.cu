@@ -40,9 +40,8 @@ struct Dim2 {
   static constexpr int LD = (N + 3) & ~3;
   static constexpr int ACC = 9 * N;   // must match gen/plan.py
   static constexpr int SAB = 12 * N;
-  static constexpr int WS = 12 * N + 2 * NF;
-  static constexpr int WARPS_RAW = (200 * 1024) / (WS * 8);
-  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
+  static constexpr int WS = 12 * N + 2 * NF;   // doubles per CTA (one element)
+  static constexpr int W = 4;                  // warps per CTA sharing the element
 };
 
 // Reference face tangents t̂1 = v̂b - v̂a, t̂2 = v̂c - v̂a (reading G9).
@@ -149,18 +148,79 @@ __device__ __forceinline__ void load_elem(const double *__restrict__ F, int64_t 
   }
 }
 
-// lift of the two face fields A, B (face f) into the accumulator:
-// acc[m][β] += t̂1_m Σ_γ L_f[β,γ] A_γ + t̂2_m Σ_γ L_f[β,γ] B_γ
-__device__ __forceinline__ void run_lift2(const DevProg &p, const double *AB, int N, int NF, double *acc, int f,
-                                          int lane) {
+// CTA-cooperative program execution for the high-order path: the W warps of a
+// CTA share one element workspace and split each DAG level's passes of 32 rows;
+// levels are separated by CTA barriers (all threads see the same sync flags).
+template <int W>
+__device__ __forceinline__ void cta_assign(const DevProg &p, double *s, int warp, int lane) {
+  int ps = 0;
+  while (ps < p.npass) {
+    int pe = ps;
+    while (!__ldg(p.sync + pe)) ++pe;               // last pass of this level
+    for (int q = ps + warp; q <= pe; q += W) {
+      const int row = q * 32 + lane;
+      const unsigned d = __ldg(p.dst + row);
+      if (d != 0xFFFFu) {
+        const int c = __ldg(p.cnt + row);
+        const int o = __ldg(p.off + q) * 32 + lane;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < c; ++t) acc = fma(__ldg(p.coef + o + 32 * t), s[__ldg(p.src + o + 32 * t)], acc);
+        s[d] = acc;
+      }
+    }
+    __syncthreads();
+    ps = pe + 1;
+  }
+}
+
+template <int F, int W>
+__device__ __forceinline__ void cta_trace_f(const DevProg &p, const double *sY, int N, int NF, double *out, int warp,
+                                            int lane) {
+  for (int q = warp; q < p.npass; q += W) {
+    const int row = q * 32 + lane;
+    const unsigned g = __ldg(p.dst + row);
+    if (g != 0xFFFFu) {
+      const int c = __ldg(p.cnt + row);
+      const int o = __ldg(p.off + q) * 32 + lane;
+      double t1 = 0.0, t2 = 0.0;
+#pragma unroll 4
+      for (int t = 0; t < c; ++t) {
+        double a1, a2;
+        tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
+        const double cf = __ldg(p.coef + o + 32 * t);
+        t1 = fma(cf, a1, t1);
+        t2 = fma(cf, a2, t2);
+      }
+      out[g] = t1;
+      out[NF + g] = t2;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void cta_trace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *out,
+                                          int warp, int lane) {
+  switch (f) {
+    case 0: cta_trace_f<0, W>(pr.trace[0], sY, N, NF, out, warp, lane); break;
+    case 1: cta_trace_f<1, W>(pr.trace[1], sY, N, NF, out, warp, lane); break;
+    case 2: cta_trace_f<2, W>(pr.trace[2], sY, N, NF, out, warp, lane); break;
+    default: cta_trace_f<3, W>(pr.trace[3], sY, N, NF, out, warp, lane); break;
+  }
+}
+
+// acc[m][β] += t̂1_m Σ_γ L_f[β,γ] A_γ + t̂2_m Σ_γ L_f[β,γ] B_γ  (rows split over the W warps)
+template <int W>
+__device__ __forceinline__ void cta_lift2(const DevProg &p, const double *AB, int N, int NF, double *acc, int f,
+                                          int warp, int lane) {
   const double a0 = kT1[f][0], a1 = kT1[f][1], a2 = kT1[f][2];
   const double b0 = kT2[f][0], b1 = kT2[f][1], b2 = kT2[f][2];
-  for (int ps = 0; ps < p.npass; ++ps) {
-    const int row = ps * 32 + lane;
+  for (int q = warp; q < p.npass; q += W) {
+    const int row = q * 32 + lane;
     const unsigned b = __ldg(p.dst + row);
     if (b != 0xFFFFu) {
       const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + ps) * 32 + lane;
+      const int o = __ldg(p.off + q) * 32 + lane;
       double la = 0.0, lb = 0.0;
 #pragma unroll 4
       for (int t = 0; t < c; ++t) {
@@ -176,59 +236,68 @@ __device__ __forceinline__ void run_lift2(const DevProg &p, const double *AB, in
   }
 }
 
-// Warp-per-element stage kernel for p > kLanePmax (trace-buffer scheme).  One
-// warp owns one element at a time.  Own and neighbour traces of Ŷ are read from
-// the trace buffer tr[e][f][k][γ] written by the stage that last updated Ŷ; the
-// lift acts on the two face fields A = -sf D₂ (+ upwind), B = sf D₁ (+ upwind),
-// acc_m += t̂1_m L_f(A) + t̂2_m L_f(B); after the update the warp writes the
-// traces of the updated field for the next stage.
+template <int LD, int N>
+__device__ __forceinline__ void cta_load_elem(const double *__restrict__ F, int64_t e, int64_t cs, double *s, int tid,
+                                              int nthreads) {
+  for (int c = 0; c < 3; ++c) {
+    const double *src = F + c * cs + e * LD;
+    for (int i = tid; i < N; i += nthreads) s[c * N + i] = __ldg(src + i);
+  }
+}
+
+// High-order stage kernel (p > kLanePmax), trace-buffer scheme.  A CTA of W warps
+// owns one element at a time (grid-stride).  Own and neighbour traces of Ŷ come
+// from the trace buffer tr[e][f][k][γ] written by the stage that last updated Ŷ;
+// the lift acts on the two face fields A = -sf D₂ (+ upwind), B = sf D₁ (+ upwind),
+// acc_m += t̂1_m L_f(A) + t̂2_m L_f(B); after the update the CTA writes the traces
+// of the updated field for the next stage.
 template <int P, bool UP>
-__global__ void __launch_bounds__(Dim2<P>::WARPS * 32)
+__global__ void __launch_bounds__(Dim2<P>::W * 32)
     stage2_kernel(StageArgs a, DevProgs pr, const double *__restrict__ trY, double *__restrict__ trOut) {
   using D = Dim2<P>;
-  constexpr int N = D::N, NF = D::NF, LD = D::LD;
+  constexpr int N = D::N, NF = D::NF, LD = D::LD, W = D::W, NT = 32 * D::W;
   extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *s = smem + warp * D::WS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  double *s = smem;
   double *sACC = s + D::ACC;
   double *sAB = s + D::SAB;
   const int64_t cs = a.n_tet * LD;
   const bool stageE = a.stage == STAGE_E;
   const bool upd = a.out_mode == OUT_UPDATE;
   const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
-  for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < a.n_tet; e += (int64_t)gridDim.x * D::WARPS) {
-    load_elem<LD, N>(a.Y, e, cs, s, lane);
-    __syncwarp();
+  for (int64_t e = blockIdx.x; e < a.n_tet; e += gridDim.x) {
+    cta_load_elem<LD, N>(a.Y, e, cs, s, tid, NT);
+    __syncthreads();
     if (a.do_curl) {
-      run_assign(pr.curl, s, lane);
+      cta_assign<W>(pr.curl, s, warp, lane);
     } else {
-      for (int i = lane; i < 3 * N; i += 32) sACC[i] = 0.0;
+      for (int i = tid; i < 3 * N; i += NT) sACC[i] = 0.0;
+      __syncthreads();
     }
-    __syncwarp();
     // Ŷ is dead (traces come from the buffer): stage X in its slots
-    if (upd) load_elem<LD, N>(a.X, e, cs, s, lane);
+    if (upd) cta_load_elem<LD, N>(a.X, e, cs, s, tid, NT);
     const Geo g = a.geo[e];
     if (a.do_flux) {
       const double sgn = g.detF > 0 ? 1.0 : -1.0;
       for (int f = 0; f < 4; ++f) {
         const int nb = a.nbr[4 * e + f];
         const int gf = a.nbrf[4 * e + f];
-        double w = 0.5, k = 0.0;
+        double w = 0.5, kk = 0.0;
         if (UP) {
           const double Zm = g.Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
           if (stageE) {
             w = Zp / (Zm + Zp);
-            k = 1.0 / (Zm + Zp);
+            kk = 1.0 / (Zm + Zp);
           } else {
             const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
             w = Yp / (Ym + Yp);
-            k = 1.0 / (Ym + Yp);
+            kk = 1.0 / (Ym + Yp);
           }
         }
         const double sf = (f & 1) ? -1.0 : 1.0;
         const double *to = trY + (e * 4 + f) * 2 * NF;
         const double *tn = nb >= 0 ? trY + ((int64_t)nb * 4 + gf) * 2 * NF : nullptr;
-        for (int gm = lane; gm < NF; gm += 32) {
+        for (int gm = tid; gm < NF; gm += NT) {
           const double o1 = __ldg(to + gm), o2 = __ldg(to + NF + gm);
           const double n1 = nb >= 0 ? __ldg(tn + gm) : mirrorY * o1;
           const double n2 = nb >= 0 ? __ldg(tn + NF + gm) : mirrorY * o2;
@@ -245,7 +314,7 @@ __global__ void __launch_bounds__(Dim2<P>::WARPS * 32)
               xn1 = mirrorX * xo1;
               xn2 = mirrorX * xo2;
             }
-            const double j1 = k * (xn1 - xo1), j2 = k * (xn2 - xo2);
+            const double j1 = kk * (xn1 - xo1), j2 = kk * (xn2 - xo2);
             const double *M = a.fmet + 12 * e + 3 * f;
             const double ps = (stageE ? 1.0 : -1.0) * sgn;
             A += ps * (j1 * M[0] + j2 * M[1]);
@@ -254,14 +323,14 @@ __global__ void __launch_bounds__(Dim2<P>::WARPS * 32)
           sAB[gm] = A;
           sAB[NF + gm] = B;
         }
-        __syncwarp();
-        run_lift2(pr.lift[f], sAB, N, NF, sACC, f, lane);
-        __syncwarp();
+        __syncthreads();
+        cta_lift2<W>(pr.lift[f], sAB, N, NF, sACC, f, warp, lane);
+        __syncthreads();
       }
     }
     // S2 + S6: inverse mass with geometry, then update (X staged in slots [0,3N)) or write
     const double cm = stageE ? g.inv_eps : -g.inv_mu;
-    for (int b = lane; b < N; b += 32) {
+    for (int b = tid; b < N; b += NT) {
       const double v0 = sACC[b], v1 = sACC[N + b], v2 = sACC[2 * N + b];
       const double x0 = cm * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
       const double x1 = cm * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
@@ -285,29 +354,27 @@ __global__ void __launch_bounds__(Dim2<P>::WARPS * 32)
         a.dX[2 * cs + o] += x2;
       }
     }
-    __syncwarp();
-    if (upd && trOut) {
-      for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, trOut + (e * 4 + f) * 2 * NF, lane);
-    }
-    __syncwarp();
+    __syncthreads();
+    if (upd && trOut)
+      for (int f = 0; f < 4; ++f) cta_trace<W>(pr, f, s, N, NF, trOut + (e * 4 + f) * 2 * NF, warp, lane);
+    __syncthreads();
   }
 }
 
-// tangential traces of a field for all elements -> tr[e][f][k][γ] (warp path layout)
+// tangential traces of a field for all elements -> tr[e][f][k][γ] (high-order layout)
 template <int P>
-__global__ void __launch_bounds__(Dim2<P>::WARPS * 32) trace2_kernel(const double *__restrict__ X, double *tr,
-                                                                      int64_t n_tet, DevProgs pr) {
+__global__ void __launch_bounds__(Dim2<P>::W * 32) trace2_kernel(const double *__restrict__ X, double *tr,
+                                                                  int64_t n_tet, DevProgs pr) {
   using D = Dim2<P>;
-  constexpr int N = D::N, NF = D::NF, LD = D::LD;
+  constexpr int N = D::N, NF = D::NF, LD = D::LD, W = D::W, NT = 32 * D::W;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double *s = smem + warp * D::WS;
   const int64_t cs = n_tet * LD;
-  for (int64_t e = (int64_t)blockIdx.x * D::WARPS + warp; e < n_tet; e += (int64_t)gridDim.x * D::WARPS) {
-    load_elem<LD, N>(X, e, cs, s, lane);
-    __syncwarp();
-    for (int f = 0; f < 4; ++f) run_trace(pr, f, s, N, NF, tr + (e * 4 + f) * 2 * NF, lane);
-    __syncwarp();
+  for (int64_t e = blockIdx.x; e < n_tet; e += gridDim.x) {
+    cta_load_elem<LD, N>(X, e, cs, smem, threadIdx.x, NT);
+    __syncthreads();
+    for (int f = 0; f < 4; ++f) cta_trace<W>(pr, f, smem, N, NF, tr + (e * 4 + f) * 2 * NF, warp, lane);
+    __syncthreads();
   }
 }
 
@@ -370,16 +437,15 @@ __global__ void sum_kernel(const double *partial, int n, double *out) {
 template <int P>
 static dgm_status launch_stage2_p(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
   using D = Dim2<P>;
-  const size_t smem = sizeof(double) * D::WS * D::WARPS;
+  const size_t smem = sizeof(double) * D::WS;
   auto go = [&](auto kernel) {
     int occ = 0;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, D::WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, D::W * 32, smem);
     if (occ < 1) occ = 1;
-    int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
     int64_t grid = (int64_t)c->sms * occ;
-    if (grid > need) grid = need;
-    kernel<<<(unsigned)grid, D::WARPS * 32, smem, st>>>(a, c->progs, trY, trOut);
+    if (grid > c->n_tet) grid = c->n_tet;
+    kernel<<<(unsigned)grid, D::W * 32, smem, st>>>(a, c->progs, trY, trOut);
   };
   if (a.upwind) go(stage2_kernel<P, true>);
   else go(stage2_kernel<P, false>);
@@ -392,15 +458,14 @@ static dgm_status launch_stage2_p(dgm_ctx *c, const StageArgs &a, const double *
 template <int P>
 static dgm_status launch_trace2_p(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
   using D = Dim2<P>;
-  const size_t smem = sizeof(double) * D::WS * D::WARPS;
+  const size_t smem = sizeof(double) * D::WS;
   int occ = 0;
   cudaFuncSetAttribute(trace2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace2_kernel<P>, D::WARPS * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace2_kernel<P>, D::W * 32, smem);
   if (occ < 1) occ = 1;
-  int64_t need = (c->n_tet + D::WARPS - 1) / D::WARPS;
   int64_t grid = (int64_t)c->sms * occ;
-  if (grid > need) grid = need;
-  trace2_kernel<P><<<(unsigned)grid, D::WARPS * 32, smem, st>>>(X, tr, c->n_tet, c->progs);
+  if (grid > c->n_tet) grid = c->n_tet;
+  trace2_kernel<P><<<(unsigned)grid, D::W * 32, smem, st>>>(X, tr, c->n_tet, c->progs);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("trace2_kernel: ") + cudaGetErrorString(e));
