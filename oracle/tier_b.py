@@ -156,3 +156,115 @@ class TierB:
         qE = np.einsum("ltn,tlm,mtn->tn", E, Ginv, E) @ norms
         qH = np.einsum("ltn,tlm,mtn->tn", H, Ginv, H) @ norms
         return 0.5 * float(np.sum(w * (self.eps * qE + self.mu * qH)))
+
+
+class SubsetEval:
+    """Tier-B evaluation restricted to a few elements of a large mesh (for the
+    full-size sampled parity tests): the operator at element T
+    needs T's coefficients and its face neighbours' traces only, so the fields
+    are fetched through ``get(idx) -> (E[:, idx], H[:, idx])`` for the small set
+    of elements involved.  Same formulas as TierB (shared methods, same tables)."""
+
+    def __init__(self, B: TierB):
+        self.B = B
+
+    def apply(self, get, elems, which="both"):
+        """(dE, dH) at ``elems`` for the fields provided by ``get``."""
+        B = self.B
+        elems = np.asarray(elems)
+        ring = np.unique(np.concatenate([elems, B.nbr[elems][B.nbr[elems] >= 0]]))
+        E, H = get(ring)
+        return self._apply_on(ring, E, H, elems, which)
+
+    def _apply_on(self, ring, E, H, elems, which):
+        B = self.B
+        pos = {int(t): q for q, t in enumerate(ring)}
+        li = np.array([pos[int(t)] for t in elems])
+        R = B.R
+        norms = R["norms"]
+        out = {}
+        # traces of every ring element (own and neighbour copies come from here)
+        def traces(Y):
+            Tr = R["Tr"]
+            t = np.empty((Y.shape[1], 4, 2, Tr.shape[2]))
+            for f in range(4):
+                for k in range(2):
+                    t[:, f, k] = np.einsum("m,mtn->tn", B.that[f, k], Y) @ Tr[f]
+            return t
+        trE, trH = traces(E), traces(H)
+        nb = B.nbr[elems]
+        nf = B.nbr_face[elems].astype(np.int64)
+        pec = B.pec[elems]
+        gat = lambda tr, sgn: _gather(tr, nb, nf, pos, pec, li, sgn)
+        Z = B.Z
+        Zm = Z[elems][:, None]
+        Zp = np.where(pec, Zm, Z[np.where(nb >= 0, nb, elems[:, None])])
+        G = B.Gp[elems]
+        sub_B = _SubView(B, elems)
+        if which in ("both", "E"):
+            acc = np.stack([(H[c2][li] @ R["D"][d1].T) - (H[c1][li] @ R["D"][d2].T)
+                            for (d1, c2, d2, c1) in ((1, 2, 2, 1), (2, 0, 0, 2), (0, 1, 1, 0))])
+            Hp = gat(trH, 1.0)
+            wH = (Zp / (Zm + Zp))[:, :, None, None] if B.flux == "upwind" else 0.5
+            Rr = sub_B._lift_cross(wH * (Hp - trH[li]))
+            if B.flux == "upwind":
+                Ep = gat(trE, -1.0)
+                Rr += B.sgn[elems][None, :, None] * sub_B._lift_tan((1.0 / (Zm + Zp))[:, :, None, None] * (Ep - trE[li]))
+            acc = acc + Rr / norms[None, None, :]
+            out["dE"] = np.einsum("tlm,mtn->ltn", G, acc) / B.eps[elems][None, :, None]
+        if which in ("both", "H"):
+            acc = np.stack([(E[c2][li] @ R["D"][d1].T) - (E[c1][li] @ R["D"][d2].T)
+                            for (d1, c2, d2, c1) in ((1, 2, 2, 1), (2, 0, 0, 2), (0, 1, 1, 0))])
+            Ep = gat(trE, -1.0)
+            Ym, Yp = 1.0 / Zm, 1.0 / Zp
+            wE = (Yp / (Ym + Yp))[:, :, None, None] if B.flux == "upwind" else 0.5
+            Rr = sub_B._lift_cross(wE * (Ep - trE[li]))
+            if B.flux == "upwind":
+                Hp = gat(trH, 1.0)
+                Rr -= B.sgn[elems][None, :, None] * sub_B._lift_tan((1.0 / (Ym + Yp))[:, :, None, None] * (Hp - trH[li]))
+            acc = acc + Rr / norms[None, None, :]
+            out["dH"] = -np.einsum("tlm,mtn->ltn", G, acc) / B.mu[elems][None, :, None]
+        return out
+
+    def step(self, get, elems, dt):
+        """One symplectic-Euler step evaluated at ``elems``:
+        H is advanced on the 1-ring of elems (which needs E on the 2-ring), then E
+        at elems.  Returns (E_new, H_new) at elems."""
+        B = self.B
+        elems = np.asarray(elems)
+        ring1 = np.unique(np.concatenate([elems, B.nbr[elems][B.nbr[elems] >= 0]]))
+        ring2 = np.unique(np.concatenate([ring1, B.nbr[ring1][B.nbr[ring1] >= 0]]))
+        E2, H2 = get(ring2)
+        pos2 = {int(t): q for q, t in enumerate(ring2)}
+        i1 = np.array([pos2[int(t)] for t in ring1])
+        dH1 = self._apply_on(ring2, E2, H2, ring1, "H")["dH"]
+        H1 = H2[:, i1] + dt * dH1
+        E1 = E2[:, i1]
+        pos1 = {int(t): q for q, t in enumerate(ring1)}
+        i0 = np.array([pos1[int(t)] for t in elems])
+        dE0 = self._apply_on(ring1, E1, H1, elems, "E")["dE"]
+        return E1[:, i0] + dt * dE0, H1[:, i0]
+
+
+def _gather(tr, nb, nf, pos, pec, li, sgn):
+    """Neighbour-face traces for the selected elements (PEC: mirror of own)."""
+    n = nb.shape[0]
+    out = np.empty((n, 4) + tr.shape[2:])
+    for t in range(n):
+        for f in range(4):
+            if pec[t, f]:
+                out[t, f] = sgn * tr[li[t], f]
+            else:
+                out[t, f] = tr[pos[int(nb[t, f])], int(nf[t, f])]
+    return out
+
+
+class _SubView:
+    """Lift helpers of TierB applied to a subset of elements (same formulas)."""
+
+    def __init__(self, B, elems):
+        self.R, self.that, self.M = B.R, B.that, B.M[elems]
+        self.n_tet, self.N = len(elems), B.N
+
+    _lift_cross = TierB._lift_cross
+    _lift_tan = TierB._lift_tan

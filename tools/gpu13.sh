@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.build()"
+for c in C3; do python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${c}_x.json 2>&1; python -c "
+import json,sys; d=json.loads(open('gpurun_out/bench_${c}_x.json').read().strip().splitlines()[-1]); print('$c', d['value'], d['ms_per_step'], d['roofline']['frac'])"; done
