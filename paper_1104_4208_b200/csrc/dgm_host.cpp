@@ -263,6 +263,8 @@ dgm_status upload_impl(dgm_ctx *c) {
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
   for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);
+  for (int f = 0; f < 4; ++f)
+    bytes += prog_bytes(hs.strace[f].prog) + prog_bytes(hs.slift[f].prog) + 2 * (((size_t)c->N * 2 + 255) & ~size_t(255));
   std::vector<char> buf(bytes, 0);
   CUDA_TRY(c, cudaMalloc(&c->d_blob, bytes));
   size_t off = 0;
@@ -271,6 +273,20 @@ dgm_status upload_impl(dgm_ctx *c) {
   for (int f = 0; f < 4; ++f) {
     c->progs.trace[f] = stage_prog(hs.trace[f], buf, off, base);
     c->progs.lift[f] = stage_prog(hs.lift[f], buf, off, base);
+  }
+  auto stage_sprog = [&](const dgm::HostSProg &h, int nout) {
+    dgm::DevSProg d;
+    d.prog = stage_prog(h.prog, buf, off, base);
+    d.n_in = h.n_in;
+    d.n_scr = h.n_scr;
+    std::memcpy(buf.data() + off, h.out, nout * 2);
+    d.out = (const uint16_t *)(base + off);
+    off += ((size_t)nout * 2 + 255) & ~size_t(255);
+    return d;
+  };
+  for (int f = 0; f < 4; ++f) {
+    c->progs.strace[f] = stage_sprog(hs.strace[f], c->NF);
+    c->progs.slift[f] = stage_sprog(hs.slift[f], c->N);
   }
   std::memcpy(buf.data() + off, hs.norms, c->N * 8);
   c->progs.norms = (const double *)(base + off);

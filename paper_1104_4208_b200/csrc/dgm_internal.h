@@ -20,11 +20,20 @@ struct HostProg {
   const int32_t *off;
   const uint8_t *sync;
 };
+// staged (sum-factorised) program: stage 0 reads the n_in inputs, later stages and
+// all destinations live in an n_scr-slot scratch; out[i] = scratch slot of output i
+struct HostSProg {
+  HostProg prog;
+  int n_in, n_scr;
+  const uint16_t *out;
+};
 struct HostProgSet {
   int p, acc;
   HostProg curl;
   HostProg trace[4];
   HostProg lift[4];
+  HostSProg strace[4];
+  HostSProg slift[4];
   const double *norms;
 };
 
@@ -37,10 +46,17 @@ struct DevProg {
   const int32_t *__restrict__ off;
   const uint8_t *__restrict__ sync;
 };
+struct DevSProg {
+  DevProg prog;
+  int n_in, n_scr;
+  const uint16_t *__restrict__ out;
+};
 struct DevProgs {
   DevProg curl;
   DevProg trace[4];
   DevProg lift[4];
+  DevSProg strace[4];
+  DevSProg slift[4];
   const double *__restrict__ norms;
 };
 

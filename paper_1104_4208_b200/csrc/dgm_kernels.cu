@@ -236,6 +236,124 @@ __device__ __forceinline__ void cta_lift2(const DevProg &p, const double *AB, in
   }
 }
 
+// Staged (sum-factorised) trace of face F for both tangential components: stage 0
+// reads the volume field through tangential<F>, later stages the scratch (pairs);
+// the outputs are copied to out[0..NF) (k=1) and out[NF..2NF) (k=2).
+template <int F, int W>
+__device__ __forceinline__ void cta_strace_f(const DevSProg &sp, const double *sY, int N, int NF, double *scr,
+                                             double *out, int warp, int lane) {
+  const DevProg &p = sp.prog;
+  int ps = 0, lvl = 0;
+  while (ps < p.npass) {
+    int pe = ps;
+    while (!__ldg(p.sync + pe)) ++pe;
+    for (int q = ps + warp; q <= pe; q += W) {
+      const int row = q * 32 + lane;
+      const unsigned d = __ldg(p.dst + row);
+      if (d != 0xFFFFu) {
+        const int c = __ldg(p.cnt + row);
+        const int o = __ldg(p.off + q) * 32 + lane;
+        double t1 = 0.0, t2 = 0.0;
+        if (lvl == 0) {
+#pragma unroll 4
+          for (int t = 0; t < c; ++t) {
+            double a1, a2;
+            tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
+            const double cf = __ldg(p.coef + o + 32 * t);
+            t1 = fma(cf, a1, t1);
+            t2 = fma(cf, a2, t2);
+          }
+        } else {
+#pragma unroll 4
+          for (int t = 0; t < c; ++t) {
+            const int sr = __ldg(p.src + o + 32 * t);
+            const double cf = __ldg(p.coef + o + 32 * t);
+            t1 = fma(cf, scr[2 * sr], t1);
+            t2 = fma(cf, scr[2 * sr + 1], t2);
+          }
+        }
+        scr[2 * d] = t1;
+        scr[2 * d + 1] = t2;
+      }
+    }
+    __syncthreads();
+    ps = pe + 1;
+    ++lvl;
+  }
+  for (int g = warp * 32 + lane; g < NF; g += W * 32) {
+    const int sl = __ldg(sp.out + g);
+    out[g] = scr[2 * sl];
+    out[NF + g] = scr[2 * sl + 1];
+  }
+  __syncthreads();
+}
+
+template <int W>
+__device__ __forceinline__ void cta_strace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *scr,
+                                           double *out, int warp, int lane) {
+  switch (f) {
+    case 0: cta_strace_f<0, W>(pr.strace[0], sY, N, NF, scr, out, warp, lane); break;
+    case 1: cta_strace_f<1, W>(pr.strace[1], sY, N, NF, scr, out, warp, lane); break;
+    case 2: cta_strace_f<2, W>(pr.strace[2], sY, N, NF, scr, out, warp, lane); break;
+    default: cta_strace_f<3, W>(pr.strace[3], sY, N, NF, scr, out, warp, lane); break;
+  }
+}
+
+// Staged lift of the two face fields A = AB[0..NF), B = AB[NF..2NF) into the
+// accumulator: acc[m][β] += t̂1_m L_f(A)_β + t̂2_m L_f(B)_β.
+template <int W>
+__device__ __forceinline__ void cta_slift2(const DevSProg &sp, const double *AB, int N, int NF, double *scr,
+                                           double *acc, int f, int warp, int lane) {
+  const DevProg &p = sp.prog;
+  int ps = 0, lvl = 0;
+  while (ps < p.npass) {
+    int pe = ps;
+    while (!__ldg(p.sync + pe)) ++pe;
+    for (int q = ps + warp; q <= pe; q += W) {
+      const int row = q * 32 + lane;
+      const unsigned d = __ldg(p.dst + row);
+      if (d != 0xFFFFu) {
+        const int c = __ldg(p.cnt + row);
+        const int o = __ldg(p.off + q) * 32 + lane;
+        double la = 0.0, lb = 0.0;
+        if (lvl == 0) {
+#pragma unroll 4
+          for (int t = 0; t < c; ++t) {
+            const int sr = __ldg(p.src + o + 32 * t);
+            const double cf = __ldg(p.coef + o + 32 * t);
+            la = fma(cf, AB[sr], la);
+            lb = fma(cf, AB[NF + sr], lb);
+          }
+        } else {
+#pragma unroll 4
+          for (int t = 0; t < c; ++t) {
+            const int sr = __ldg(p.src + o + 32 * t);
+            const double cf = __ldg(p.coef + o + 32 * t);
+            la = fma(cf, scr[2 * sr], la);
+            lb = fma(cf, scr[2 * sr + 1], lb);
+          }
+        }
+        scr[2 * d] = la;
+        scr[2 * d + 1] = lb;
+      }
+    }
+    __syncthreads();
+    ps = pe + 1;
+    ++lvl;
+  }
+  const double a0 = kT1[f][0], a1 = kT1[f][1], a2 = kT1[f][2];
+  const double b0 = kT2[f][0], b1 = kT2[f][1], b2 = kT2[f][2];
+  for (int b = warp * 32 + lane; b < N; b += W * 32) {
+    const int sl = __ldg(sp.out + b);
+    if (sl == 0xFFFF) continue;
+    const double la = scr[2 * sl], lb = scr[2 * sl + 1];
+    acc[b] += a0 * la + b0 * lb;
+    acc[N + b] += a1 * la + b1 * lb;
+    acc[2 * N + b] += a2 * la + b2 * lb;
+  }
+  __syncthreads();
+}
+
 template <int LD, int N>
 __device__ __forceinline__ void cta_load_elem(const double *__restrict__ F, int64_t e, int64_t cs, double *s, int tid,
                                               int nthreads) {
@@ -324,8 +442,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32)
           sAB[NF + gm] = B;
         }
         __syncthreads();
-        cta_lift2<W>(pr.lift[f], sAB, N, NF, sACC, f, warp, lane);
-        __syncthreads();
+        cta_slift2<W>(pr.slift[f], sAB, N, NF, s + 3 * N, sACC, f, warp, lane);
       }
     }
     // S2 + S6: inverse mass with geometry, then update (X staged in slots [0,3N)) or write
@@ -356,7 +473,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32)
     }
     __syncthreads();
     if (upd && trOut)
-      for (int f = 0; f < 4; ++f) cta_trace<W>(pr, f, s, N, NF, trOut + (e * 4 + f) * 2 * NF, warp, lane);
+      for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, s, N, NF, s + 3 * N, trOut + (e * 4 + f) * 2 * NF, warp, lane);
     __syncthreads();
   }
 }
@@ -373,8 +490,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32) trace2_kernel(const double *_
   for (int64_t e = blockIdx.x; e < n_tet; e += gridDim.x) {
     cta_load_elem<LD, N>(X, e, cs, smem, threadIdx.x, NT);
     __syncthreads();
-    for (int f = 0; f < 4; ++f) cta_trace<W>(pr, f, smem, N, NF, tr + (e * 4 + f) * 2 * NF, warp, lane);
-    __syncthreads();
+    for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, smem, N, NF, smem + 3 * N, tr + (e * 4 + f) * 2 * NF, warp, lane);
   }
 }
 

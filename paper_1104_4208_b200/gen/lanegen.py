@@ -99,57 +99,58 @@ def gen_sweep(p, d, ct):
 
 
 def gen_trace(p, f, ct):
-    _, T = plan.load(p)
-    N, NF = plan.n_modes(p), plan.n_face_modes(p)
+    """Face-f trace of one scalar field (sum-factorised staged program of
+    gen/facetrace.py): out[γ·os] = Σ_α Tr_f[α,γ] (a[α] - b[α]) (b only on face 0)."""
+    from . import facetrace
+    sp = facetrace.trace_program(p, f)
+    N = sp.n_in
     sub = f == 0
     sig = "const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ out, int os" if sub else \
           "const double *__restrict__ a, double *__restrict__ out, int os"
     out = [f"__device__ __noinline__ void lane_trace_p{p}_f{f}({sig}) {{"]
-    acc = {g: [] for g in range(NF)}
-    lines = []
-    for al in range(N):
-        nz = [(g, T[f][al][g]) for g in range(NF) if T[f][al][g] != 0]
-        if not nz:
-            continue
+    used = sorted({sl for _, t in sp.stages[0] for sl, _ in t})
+    for al in used:
         if sub:
-            lines.append(f"  const double a{al} = a[{al * S}] - b[{al * S}];")
+            out.append(f"  const double x{al} = a[{al * S}] - b[{al * S}];")
         else:
-            lines.append(f"  const double a{al} = a[{al * S}];")
-        for g, c in nz:
-            acc[g].append((float(c), f"a{al}"))
-    out += lines
-    for g in range(NF):
-        out.append(f"  out[{g} * os] = {_chain(ct, acc[g])};")
+            out.append(f"  const double x{al} = a[{al * S}];")
+    for st in sp.stages:
+        for d, terms in st:
+            out.append(f"  const double x{d} = {_chain(ct, [(float(c), f'x{sl}') for sl, c in terms])};")
+    for g, sl in enumerate(sp.out_slots):
+        out.append(f"  out[{g} * os] = x{sl};")
     out.append("}")
     return "\n".join(out)
 
 
 def gen_lift(p, f, ct):
-    """o[β] += L_f(q)[β].  Face 0 (t̂1 = (-1,1,0), t̂2 = (-1,0,1)) also subtracts
-    L from component 0, which both halves share: the two halves take turns."""
-    _, T = plan.load(p)
-    n3, n2 = plan.norms3(p), plan.norms2(p)
-    N, NF = plan.n_modes(p), plan.n_face_modes(p)
+    """o[β] += L_f(q)[β] (sum-factorised staged lift, ‖ψ‖²/‖φ‖² folded in).  Face 0
+    (t̂1 = (-1,1,0), t̂2 = (-1,0,1)) also subtracts L from component 0, which both
+    halves share: the two halves take turns."""
+    from . import facetrace
+    sp = facetrace.lift_program(p, f)
+    NF = sp.n_in
     qargs = ", ".join(f"double q{g}" for g in range(NF))
     if f == 0:
         out = [f"__device__ __noinline__ void lane_lift_p{p}_f0({qargs}, double *__restrict__ o, double *__restrict__ o0, int h) {{"]
     else:
         out = [f"__device__ __noinline__ void lane_lift_p{p}_f{f}({qargs}, double *__restrict__ o) {{"]
-    rows = []
-    for b in range(N):
-        terms = [(float(T[f][b][g] * n2[g] / n3[b]), f"q{g}") for g in range(NF) if T[f][b][g] != 0]
-        if terms:
-            rows.append(b)
-            out.append(f"  const double L{b} = {_chain(ct, terms)};")
-            out.append(f"  o[{b * S}] += L{b};")
+    for g in range(NF):
+        out.append(f"  const double x{g} = q{g};")
+    for st in sp.stages:
+        for d, terms in st:
+            out.append(f"  const double x{d} = {_chain(ct, [(float(c), f'x{sl}') for sl, c in terms])};")
+    rows = [(b, sl) for b, sl in enumerate(sp.out_slots) if sl >= 0]
+    for b, sl in rows:
+        out.append(f"  o[{b * S}] += x{sl};")
     if f == 0:
         out.append("  __syncwarp();")
         out.append("  if (h == 0) {")
-        out += [f"    o0[{b * S}] -= L{b};" for b in rows]
+        out += [f"    o0[{b * S}] -= x{sl};" for b, sl in rows]
         out.append("  }")
         out.append("  __syncwarp();")
         out.append("  if (h == 1) {")
-        out += [f"    o0[{b * S}] -= L{b};" for b in rows]
+        out += [f"    o0[{b * S}] -= x{sl};" for b, sl in rows]
         out.append("  }")
     out.append("}")
     return "\n".join(out)

@@ -223,6 +223,72 @@ def stats(p):
 
 
 # ---------------------------------------------------------------------------
+# sum-factorised (staged) trace and lift programs, see gen/facetrace.py
+def staged_passes(sp):
+    """ELL passes of a staged program: one DAG level per stage.  Stage 0 reads
+    the program inputs (slot < n_in, indexed directly); later stages read the
+    scratch (slot - n_in); destinations are scratch slots.  Returns the pass
+    arrays plus ``out`` (scratch slot of each output, 0xFFFF if none), n_in, n_scr."""
+    n_in = sp.n_in
+    levels = []
+    for lv, st in enumerate(sp.stages):
+        rows = []
+        for d, terms in st:
+            assert d >= n_in
+            if lv == 0:
+                assert all(sl < n_in for sl, _ in terms)
+                rows.append((d - n_in, [(sl, c) for sl, c in terms]))
+            else:
+                assert all(sl >= n_in for sl, _ in terms)
+                rows.append((d - n_in, [(sl - n_in, c) for sl, c in terms]))
+        levels.append(rows)
+    out = _to_passes(levels)
+    out["out"] = np.array([(o - n_in) if o >= 0 else 0xFFFF for o in sp.out_slots], np.uint16)
+    out["n_in"] = n_in
+    out["n_scr"] = sp.n_slots - n_in
+    return out
+
+
+@lru_cache(maxsize=None)
+def strace_passes(p, f):
+    from . import facetrace
+    return staged_passes(facetrace.trace_program(p, f))
+
+
+@lru_cache(maxsize=None)
+def slift_passes(p, f):
+    from . import facetrace
+    return staged_passes(facetrace.lift_program(p, f))
+
+
+def exec_staged(sp_passes, inputs):
+    """numpy executor of a staged ELL program on inputs [n_in, n_elem] -> outputs."""
+    P = sp_passes
+    n_el = inputs.shape[1]
+    scr = np.zeros((P["n_scr"], n_el))
+    level_start = 0
+    lvl = 0
+    for ps in range(len(P["sync"])):
+        o0 = P["pass_off"][ps]
+        res = []
+        for l in range(WARP):
+            d = P["dst"][ps * WARP + l]
+            if d == 0xFFFF:
+                continue
+            acc = np.zeros(n_el)
+            for t in range(P["cnt"][ps * WARP + l]):
+                q = (o0 + t) * WARP + l
+                src = inputs if lvl == 0 else scr
+                acc = acc + P["coef"][q] * src[P["src"][q]]
+            res.append((d, acc))
+        for d, acc in res:
+            scr[d] = acc
+        if P["sync"][ps]:
+            lvl += 1
+    return np.stack([scr[o] if o != 0xFFFF else np.zeros(n_el) for o in P["out"]])
+
+
+# ---------------------------------------------------------------------------
 # numpy executors of the programs (used by the CPU tests against the oracle)
 def exec_passes(prog, slots, mode="assign"):
     """Execute an ELL program on slots [n_slots, n_elem] in place (vectorised over elements)."""
@@ -329,9 +395,19 @@ def emit_c(path, pmax=PMAX):
             s, ini = _emit_prog(f"lift_p{p}_f{f}", lift_tables(p)[f])
             out.append(s)
             li_inits.append(ini)
+        st_inits, sl_inits = [], []
+        for f in range(4):
+            for kind, fn, lst in (("strace", strace_passes, st_inits), ("slift", slift_passes, sl_inits)):
+                sp = fn(p, f)
+                name = f"{kind}_p{p}_f{f}"
+                s_, ini = _emit_prog(name, sp)
+                out.append(s_)
+                out.append(_c_array(f"{name}_out", "uint16_t", sp["out"], str))
+                lst.append(f"{{{ini}, {sp['n_in']}, {sp['n_scr']}, {name}_out}}")
         nrm = np.array([float(x) for x in norms3(p)])
         out.append(_c_array(f"norms_p{p}", "double", nrm, lambda x: float(x).hex()))
-        sets.append(f"{{{p}, {cp['ACC']}, {c_init}, {{{', '.join(tr_inits)}}}, {{{', '.join(li_inits)}}}, norms_p{p}}}")
+        sets.append(f"{{{p}, {cp['ACC']}, {c_init}, {{{', '.join(tr_inits)}}}, {{{', '.join(li_inits)}}}, "
+                    f"{{{', '.join(st_inits)}}}, {{{', '.join(sl_inits)}}}, norms_p{p}}}")
     out.append("static const HostProgSet kHostProgs[] = {\n  " + ",\n  ".join(sets) + "\n};\n")
     with open(path, "w") as f:
         f.write("".join(out))

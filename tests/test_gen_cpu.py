@@ -91,3 +91,43 @@ def test_printed_2d_relations_hold():
             scale = 1e4 * (1 + i + j) ** 4
             assert np.abs(rx).max() < 1e-5 * scale
             assert np.abs(ry).max() < 1e-5 * scale
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 5])
+def test_sum_factorised_traces_exact(p):
+    """The sum-factorised (tensor-product) face traces and lifts of gen/facetrace.py
+     multiply out, in exact rational arithmetic, to the exact
+    restriction matrices Tr_f (and Tr_fᵀ‖ψ‖²/‖φ‖²)."""
+    from paper_1104_4208_b200.gen import facetrace as FT
+    _, T = plan.load(p)
+    N, NF = plan.n_modes(p), plan.n_face_modes(p)
+    n2, n3 = plan.norms2(p), plan.norms3(p)
+    for f in range(4):
+        M = FT.compose(FT.trace_program(p, f), NF)
+        assert all(M[a][g] == T[f][a][g] for a in range(N) for g in range(NF))
+        L = FT.compose(FT.lift_program(p, f), N)
+        assert all(L[g][b] == T[f][b][g] * n2[g] / n3[b] for b in range(N) for g in range(NF))
+
+
+def test_sum_factorised_cost():
+    """Cost of the factorised traces vs the dense restriction nonzeros (p=10 and 6)."""
+    from paper_1104_4208_b200.gen import facetrace as FT
+    for p, ratio in ((6, 1.5), (10, 2.4)):
+        fact = sum(FT.trace_program(p, f).fma_count() for f in range(4))
+        dense = sum(int(x["cnt"].sum()) for x in plan.trace_tables(p))
+        assert dense / fact > ratio, (p, fact, dense)
+
+
+@pytest.mark.parametrize("p", [3, 7, 10])
+def test_staged_programs_match_oracle(p):
+    N, NF = plan.n_modes(p), plan.n_face_modes(p)
+    R_ = ref_ops(p)
+    rng = np.random.default_rng(p)
+    a = rng.standard_normal((N, 2))
+    q = rng.standard_normal((NF, 2))
+    for f in range(4):
+        got = plan.exec_staged(plan.strace_passes(p, f), a)
+        assert np.allclose(got, (a.T @ R_["Tr"][f]).T, atol=1e-11)
+        gl = plan.exec_staged(plan.slift_passes(p, f), q)
+        wl = ((q.T * R_["fnorms"]) @ R_["Tr"][f].T / R_["norms"]).T
+        assert np.allclose(gl, wl, atol=1e-11 * np.abs(wl).max())
