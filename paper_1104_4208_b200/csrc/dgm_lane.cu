@@ -33,8 +33,10 @@ struct L2 {
   static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
   static constexpr int NF = (P + 1) * (P + 2) / 2;
   static constexpr int LD = (N + 3) & ~3;
-  static constexpr int SY = 0, SA = 3 * N;
-  static constexpr int SE = odd_up(6 * N);         // per-element stride (odd: conflict-free)
+  // per element: Ŷ (then X) with component stride LD (the padding modes are staged
+  // too, so full groups copy without predicates), then the accumulator (stride N)
+  static constexpr int SY = 0, SA = 3 * LD;
+  static constexpr int SE = odd_up(3 * LD + 3 * N);  // per-element stride (odd: conflict-free)
   static constexpr int WS = 16 * SE;               // doubles per warp
   static constexpr int J = (16 * LD + 31) / 32;    // 8-byte copies per lane per component
   static constexpr int WARPS_RAW = (200 * 1024) / (WS * 8);
@@ -96,28 +98,42 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <int N, int LD, int SE, int J>
 struct CopyMap {
   int off[J];
+  unsigned long long real;   // bit j: copy j carries a real mode (b < N); stores skip padding
+  static_assert(J <= 64, "copy mask is 64 bits");
   __device__ __forceinline__ CopyMap(int lane) {
+    real = 0;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const int i = lane + 32 * j, e = i / LD, b = i - e * LD;
-      off[j] = (b < N && e < 16) ? e * SE + b : -1;
+      off[j] = e * SE + b;
+      if (b < N && e < 16) real |= 1ull << j;
     }
   }
 };
 
 // Coalesced asynchronous load (cp.async, LDGSTS) of nel contiguous element blocks
-// per component into s[e*SE + c*N + b]; every copy of the group is in flight at once;
-// the caller waits with cp_async_wait_all + __syncwarp.
+// per component into s[e*SE + c*LD + b] (padding modes included); every copy of the
+// group is in flight at once; the caller waits with cp_async_wait_all + __syncwarp.
 template <int N, int LD, int SE, int J>
 __device__ __forceinline__ void l2_load_async(const CopyMap<N, LD, SE, J> &m, const double *__restrict__ F,
                                               int64_t e0, int nel, int64_t cs, double *s, int lane) {
-  const int lim = nel * LD;
+  if (nel == 16) {
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double *src = F + c * cs + e0 * LD + lane;
+    for (int c = 0; c < 3; ++c) {
+      const double *src = F + c * cs + e0 * LD + lane;
 #pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (m.off[j] >= 0 && lane + 32 * j < lim) cp_async8(s + c * N + m.off[j], src + 32 * j);
+      for (int j = 0; j < J; ++j)
+        if (32 * j + 31 < 16 * LD || lane + 32 * j < 16 * LD) cp_async8(s + c * LD + m.off[j], src + 32 * j);
+    }
+  } else {
+    const int lim = nel * LD - lane;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double *src = F + c * cs + e0 * LD + lane;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        if (32 * j < lim) cp_async8(s + c * LD + m.off[j], src + 32 * j);
+    }
   }
 }
 
@@ -128,17 +144,20 @@ __device__ __forceinline__ void l2_load(const CopyMap<N, LD, SE, J> &m, const do
   cp_async_wait_all();
 }
 
+// store of the real modes (padding untouched)
 template <int N, int LD, int SE, int J>
 __device__ __forceinline__ void l2_store(const CopyMap<N, LD, SE, J> &m, double *__restrict__ F, int64_t e0, int nel,
                                          int64_t cs, const double *s, int lane, bool accumulate) {
-  const int lim = nel * LD;
+  const int nj = (nel * LD - lane + 31) / 32;   // copies of this lane inside the group (nel >= 1)
+  const unsigned long long mask = nel == 16 || nj >= J ? m.real : m.real & ((1ull << nj) - 1ull);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double *dst = F + c * cs + e0 * LD + lane;
+    const double *src = s + c * LD;
 #pragma unroll
     for (int j = 0; j < J; ++j)
-      if (m.off[j] >= 0 && lane + 32 * j < lim) {
-        const double v = s[c * N + m.off[j]];
+      if ((mask >> j) & 1ull) {
+        const double v = src[m.off[j]];
         dst[32 * j] = accumulate ? dst[32 * j] + v : v;
       }
   }
@@ -159,7 +178,7 @@ __device__ __forceinline__ void l2_traces_out(const double *el, int h, double *_
 #pragma unroll 1
   for (int f = 0; f < 4; ++f) {
     const int c = tang_comp(f, h);
-    LOps<P>::trace(f, el + c * D::N, el, tr + tix<D::NF>(ge, f, h, 0), 16);
+    LOps<P>::trace(f, el + c * D::LD, el, tr + tix<D::NF>(ge, f, h, 0), 16);
   }
 }
 
@@ -191,11 +210,11 @@ __global__ void __launch_bounds__(L2<P>::WARPS * 32)
     for (int i = h; i < 3 * N; i += 2) el[D::SA + i] = 0.0;
     __syncwarp();
     if (a.do_curl) {
-      LOps<P>::sweep(0, el + csrc0 * N, el + D::SA + cdst0 * N, cs0);
+      LOps<P>::sweep(0, el + csrc0 * LD, el + D::SA + cdst0 * N, cs0);
       __syncwarp();
-      LOps<P>::sweep(1, el + csrc1 * N, el + D::SA + cdst1 * N, cs1);
+      LOps<P>::sweep(1, el + csrc1 * LD, el + D::SA + cdst1 * N, cs1);
       __syncwarp();
-      LOps<P>::sweep(2, el + csrc2 * N, el + D::SA + cdst2 * N, cs2);
+      LOps<P>::sweep(2, el + csrc2 * LD, el + D::SA + cdst2 * N, cs2);
       __syncwarp();
     }
     bool x_issued = false;
@@ -307,12 +326,12 @@ __global__ void __launch_bounds__(L2<P>::WARPS * 32)
         const double x2 = sc * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
         if (upd) {
           el[b] += x0;
-          el[N + b] += x1;
-          el[2 * N + b] += x2;
+          el[LD + b] += x1;
+          el[2 * LD + b] += x2;
         } else {
           el[b] = x0;
-          el[N + b] = x1;
-          el[2 * N + b] = x2;
+          el[LD + b] = x1;
+          el[2 * LD + b] = x2;
         }
       }
     }
