@@ -203,8 +203,17 @@ def run_ours(args, rank, world):
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
     kern = "lane_stage_kernel" if p <= 6 else "stage2_kernel"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f).get(args.config)
+        if tr and tr.get("kernel") == f"{'lane_stage_kernel' if p <= 6 else 'stage2_kernel'}<{p}>":
+            traffic = tr["dram_bytes_per_launch"]
     res["roofline"] = {"bound": "hbm", "achieved": B / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
-                       "frac": (B / per_launch_s / 1e9) / hbm, "traffic": None,
+                       "frac": (B / per_launch_s / 1e9) / hbm, "traffic": traffic,
+                       "traffic_source": "profiles/r01_traffic.json (one ncu --set full capture, bytes per launch)"
+                       if traffic is not None else None,
                        "kernel": f"{kern}<{p}>", "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
                        "launches_per_step": launches / args.steps,
                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
