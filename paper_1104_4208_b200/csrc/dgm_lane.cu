@@ -209,7 +209,12 @@ __global__ void __launch_bounds__(L2<P>::WARPS * 32)
     const bool active = e < nel;
     const int64_t ge = e0 + e;
     l2_load(cmap, a.Y, e0, nel, cs, sw, lane);
-    for (int i = h; i < 3 * N; i += 2) el[D::SA + i] = 0.0;
+    {
+      double *z = el + D::SA + h;
+#pragma unroll
+      for (int i = 0; i < (3 * N + 1) / 2; ++i)
+        if (2 * i + 1 < 3 * N || h == 0) z[2 * i] = 0.0;
+    }
     __syncwarp();
     // own and neighbour traces of this half's component (written by the stage that
     // last updated Ŷ), prefetched one face ahead
@@ -321,19 +326,25 @@ __global__ void __launch_bounds__(L2<P>::WARPS * 32)
       const Geo g = a.geo[ge];
       const double cm = stageE ? g.inv_eps : -g.inv_mu;
       const double sc = upd ? a.dt * cm : cm;
-      for (int b = h; b < N; b += 2) {
-        const double v0 = el[D::SA + b], v1 = el[D::SA + N + b], v2 = el[D::SA + 2 * N + b];
-        const double x0 = sc * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
-        const double x1 = sc * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
-        const double x2 = sc * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
-        if (upd) {
-          el[b] += x0;
-          el[LD + b] += x1;
-          el[2 * LD + b] += x2;
-        } else {
-          el[b] = x0;
-          el[LD + b] = x1;
-          el[2 * LD + b] = x2;
+      const double *ac = el + D::SA + h;
+      double *xs = el + h;
+      constexpr int UNR = N <= 40 ? (N + 1) / 2 : 4;   // full unroll only while the code stays small
+#pragma unroll UNR
+      for (int bb = 0; bb < (N + 1) / 2; ++bb) {
+        if (2 * bb + 1 < N || h == 0) {   // mode b = 2bb + h
+          const double v0 = ac[2 * bb], v1 = ac[N + 2 * bb], v2 = ac[2 * N + 2 * bb];
+          const double x0 = sc * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
+          const double x1 = sc * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
+          const double x2 = sc * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
+          if (upd) {
+            xs[2 * bb] += x0;
+            xs[LD + 2 * bb] += x1;
+            xs[2 * LD + 2 * bb] += x2;
+          } else {
+            xs[2 * bb] = x0;
+            xs[LD + 2 * bb] = x1;
+            xs[2 * LD + 2 * bb] = x2;
+          }
         }
       }
     }
