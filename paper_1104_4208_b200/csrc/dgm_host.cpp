@@ -84,6 +84,9 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_partial);
   cudaFree(c->d_E);
   cudaFree(c->d_H);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (int i = 0; i < 4; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
 }
 
@@ -367,24 +370,22 @@ dgm_status dgm_step(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps,
   return dgm_step_ex(c, E, H, dt, nsteps, 0, stream);
 }
 
-dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, int flags, void *stream) {
-  if (!c || !E || !H || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  c->launches = 0;
-  if (nsteps == 0) return DGM_OK;
-  // Each stage reads the traces of the field it does not update (own and
-  // neighbours) from the buffer written by the stage that last updated that
-  // field, and writes the traces of the field it updates.  They are recomputed
-  // at entry so that resuming from saved (E, H) is exact.  Upwind also reads
-  // the old traces of the updated field, so those buffers ping-pong.
+namespace {
+// The step sequence of dgm_step_ex.  If h_done is given it is recorded on the
+// stream right after the last H stage (H is final from then on).  If
+// before_entry is given the stream waits on it after the entry traces of E.
+dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, int flags, cudaStream_t st,
+                     cudaEvent_t before_h, cudaEvent_t h_done) {
   const bool up = c->flux == DGM_FLUX_UPWIND;
   int ce = 0, ch = 0;
   dgm_status r = DGM_OK;
   if ((flags & DGM_STEP_CONTINUE) && c->tr_valid && c->tr_E == E && c->tr_H == H) {
     ce = c->tr_ce;
     ch = c->tr_ch;
+    if (before_h) cudaStreamWaitEvent(st, before_h, 0);
   } else {
     r = dgm::launch_tb_traces(c, E, c->d_tr[0], st);
+    if (before_h) cudaStreamWaitEvent(st, before_h, 0);   // H has arrived
     if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st);
   }
   c->tr_valid = false;
@@ -393,6 +394,7 @@ dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nste
     r = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
     if (up) ch = 1 - ch;
     if (r != DGM_OK) break;
+    if (h_done && s == nsteps - 1) cudaEventRecord(h_done, st);
     double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
     r = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
     if (up) ce = 1 - ce;
@@ -406,6 +408,19 @@ dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nste
   }
   return r;
 }
+}  // namespace
+
+dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, int flags, void *stream) {
+  if (!c || !E || !H || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
+  c->launches = 0;
+  if (nsteps == 0) return DGM_OK;
+  // Each stage reads the traces of the field it does not update (own and
+  // neighbours) from the buffer written by the stage that last updated that
+  // field, and writes the traces of the field it updates.  They are recomputed
+  // at entry so that resuming from saved (E, H) is exact.  Upwind also reads
+  // the old traces of the updated field, so those buffers ping-pong.
+  return run_steps(c, E, H, dt, nsteps, flags, (cudaStream_t)stream, nullptr, nullptr);
+}
 
 dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t nsteps, void *stream) {
   if (!c || !Eh || !Hh) return dgm::set_err(c, DGM_EINVAL, "null pointer");
@@ -415,14 +430,30 @@ dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t 
     CUDA_TRY(c, cudaMalloc(&c->d_E, bytes));
     CUDA_TRY(c, cudaMalloc(&c->d_H, bytes));
   }
+  if (!c->side) {
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming));
+  }
+  c->launches = 0;
+  if (nsteps == 0) return DGM_OK;
+  // E in on the caller's stream (the entry traces of E start as soon as it lands),
+  // H in on a side stream; H back out on the side stream as soon as the last H
+  // stage is done, overlapping the last E stage; E back out last.
+  CUDA_TRY(c, cudaEventRecord(c->ev[0], st));                 // caller's prior work
+  CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[0], 0));
   CUDA_TRY(c, cudaMemcpyAsync(c->d_E, Eh, bytes, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(c, cudaMemcpyAsync(c->d_H, Hh, bytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_H, Hh, bytes, cudaMemcpyHostToDevice, c->side));
+  CUDA_TRY(c, cudaEventRecord(c->ev[1], c->side));           // H has arrived
   c->tr_valid = false;   // fresh host data
-  dgm_status s = dgm_step(c, c->d_E, c->d_H, dt, nsteps, stream);
+  dgm_status s = run_steps(c, c->d_E, c->d_H, dt, nsteps, 0, st, c->ev[1], c->ev[2]);
   if (s != DGM_OK) return s;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[2], 0));    // last H stage done
+  CUDA_TRY(c, cudaMemcpyAsync(Hh, c->d_H, bytes, cudaMemcpyDeviceToHost, c->side));
+  CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));
   CUDA_TRY(c, cudaMemcpyAsync(Eh, c->d_E, bytes, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(c, cudaMemcpyAsync(Hh, c->d_H, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
   CUDA_TRY(c, cudaStreamSynchronize(st));
+  c->tr_valid = false;   // the caller owns the host copies now
   return DGM_OK;
 }
 

@@ -105,6 +105,8 @@ struct dgm_ctx {
   double *d_partial = nullptr; // energy partial sums
   int64_t n_partial = 0;
   double *d_E = nullptr, *d_H = nullptr;   // device copies for dgm_step_host
+  cudaStream_t side = nullptr;             // dgm_step_host: H copies overlap the kernels
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
   // trace-buffer state left by the last dgm_step (for DGM_STEP_CONTINUE)
   bool tr_valid = false;

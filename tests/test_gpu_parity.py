@@ -214,3 +214,24 @@ def test_step_continue_matches_single_call(case, p):
     c.dgm_step_ex(E2, H2, 1e-3, 1, DGM_STEP_CONTINUE)
     assert c.dgm_last_launches() > 2
     assert bool((E1 == E2).all()) and bool((H1 == H2).all())
+
+
+@pytest.mark.parametrize("case,p", [("periodic-central", 4), ("pec-upwind", 3), ("mixed-upwind", 8)])
+def test_step_host_matches_device_step(case, p):
+    """dgm_step_host (host buffers, overlapped copies on a side stream) gives the
+    same bits as dgm_step on device buffers."""
+    import torch
+    periodic, flux, n = CASES[case]
+    m, rep, eps, mu = _problem(n, periodic, p, flux)
+    c = _ctx(m, rep, p, eps, mu, flux)
+    rng = np.random.default_rng(p + 40)
+    E = rng.standard_normal((3, m.n_tet, c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N))
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    Eh, Hh = Ed.cpu().pin_memory(), Hd.cpu().pin_memory()
+    c.dgm_step(Ed, Hd, 1e-3, 3)
+    c.dgm_step_host(Eh, Hh, 1e-3, 3)
+    assert torch.equal(Eh, Ed.cpu()) and torch.equal(Hh, Hd.cpu())
+    c.dgm_step_host(Eh, Hh, 1e-3, 1)
+    c.dgm_step(Ed, Hd, 1e-3, 1)
+    assert torch.equal(Eh, Ed.cpu()) and torch.equal(Hh, Hd.cpu())
