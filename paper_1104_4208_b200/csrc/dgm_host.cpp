@@ -49,7 +49,7 @@ const int kFaceVerts[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
 size_t prog_bytes(const HostProg &p) {
   size_t rows = (size_t)p.npass * 32, terms = (size_t)p.nterm * 32;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  return al(rows * 2) * 2 + al(terms * 2) + al(terms * 8) + al((p.npass + 1) * 4) + al(p.npass + 1);
+  return al(rows * 2) * 2 + al(terms * 2) + al(terms * 8) + al((p.npass + 1) * 4) + al(p.npass + 1) + al(terms * 16);
 }
 
 // Copy one program into the staging buffer at *off, return its device view.
@@ -70,6 +70,13 @@ dgm::DevProg stage_prog(const HostProg &p, std::vector<char> &buf, size_t &off, 
   d.coef = (const double *)put(p.coef, terms * 8);
   d.off = (const int32_t *)put(p.off, (p.npass + 1) * 4);
   d.sync = (const uint8_t *)put(p.sync, p.npass ? p.npass : 1);
+  std::vector<double> packed(terms * 2);
+  for (size_t q = 0; q < terms; ++q) {
+    packed[2 * q] = p.coef[q];
+    long long sv = p.src[q];
+    std::memcpy(&packed[2 * q + 1], &sv, 8);
+  }
+  d.term = (const double2 *)put(packed.data(), terms * 16);
   return d;
 }
 

@@ -45,6 +45,8 @@ struct DevProg {
   const double *__restrict__ coef;
   const int32_t *__restrict__ off;
   const uint8_t *__restrict__ sync;
+  // the same terms packed as 16-byte {coef, src} pairs: one 128-bit load per term
+  const double2 *__restrict__ term;
 };
 struct DevSProg {
   DevProg prog;

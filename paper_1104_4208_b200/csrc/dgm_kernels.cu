@@ -40,6 +40,7 @@ struct Dim2 {
   static constexpr int LD = (N + 3) & ~3;
   static constexpr int ACC = 9 * N;   // must match gen/plan.py
   static constexpr int SAB = 12 * N;
+  static constexpr int SCR = (3 * N + 1) & ~1;   // trace/lift scratch (pairs, 16-B aligned) in the dead sweep region
   static constexpr int WS = 12 * N + 2 * NF;   // doubles per CTA (one element)
   static constexpr int W = 4;                  // warps per CTA sharing the element
 };
@@ -148,6 +149,12 @@ __device__ __forceinline__ void load_elem(const double *__restrict__ F, int64_t 
   }
 }
 
+__device__ __forceinline__ void ldterm(const DevProg &p, int q, double &cf, int &src) {
+  const double2 v = __ldg(p.term + q);
+  cf = v.x;
+  src = (int)__double_as_longlong(v.y);
+}
+
 // CTA-cooperative program execution for the high-order path: the W warps of a
 // CTA share one element workspace and split each DAG level's passes of 32 rows;
 // levels are separated by CTA barriers (all threads see the same sync flags).
@@ -165,7 +172,12 @@ __device__ __forceinline__ void cta_assign(const DevProg &p, double *s, int warp
         const int o = __ldg(p.off + q) * 32 + lane;
         double acc = 0.0;
 #pragma unroll 4
-        for (int t = 0; t < c; ++t) acc = fma(__ldg(p.coef + o + 32 * t), s[__ldg(p.src + o + 32 * t)], acc);
+        for (int t = 0; t < c; ++t) {
+          double cf;
+          int sr;
+          ldterm(p, o + 32 * t, cf, sr);
+          acc = fma(cf, s[sr], acc);
+        }
         s[d] = acc;
       }
     }
@@ -257,23 +269,25 @@ __device__ __forceinline__ void cta_strace_f(const DevSProg &sp, const double *s
         if (lvl == 0) {
 #pragma unroll 4
           for (int t = 0; t < c; ++t) {
-            double a1, a2;
-            tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
-            const double cf = __ldg(p.coef + o + 32 * t);
+            double cf, a1, a2;
+            int sr;
+            ldterm(p, o + 32 * t, cf, sr);
+            tangential<F>(sY, N, sr, a1, a2);
             t1 = fma(cf, a1, t1);
             t2 = fma(cf, a2, t2);
           }
         } else {
 #pragma unroll 4
           for (int t = 0; t < c; ++t) {
-            const int sr = __ldg(p.src + o + 32 * t);
-            const double cf = __ldg(p.coef + o + 32 * t);
-            t1 = fma(cf, scr[2 * sr], t1);
-            t2 = fma(cf, scr[2 * sr + 1], t2);
+            double cf;
+            int sr;
+            ldterm(p, o + 32 * t, cf, sr);
+            const double2 v = *reinterpret_cast<const double2 *>(scr + 2 * sr);
+            t1 = fma(cf, v.x, t1);
+            t2 = fma(cf, v.y, t2);
           }
         }
-        scr[2 * d] = t1;
-        scr[2 * d + 1] = t2;
+        *reinterpret_cast<double2 *>(scr + 2 * d) = make_double2(t1, t2);
       }
     }
     __syncthreads();
@@ -319,22 +333,24 @@ __device__ __forceinline__ void cta_slift2(const DevSProg &sp, const double *AB,
         if (lvl == 0) {
 #pragma unroll 4
           for (int t = 0; t < c; ++t) {
-            const int sr = __ldg(p.src + o + 32 * t);
-            const double cf = __ldg(p.coef + o + 32 * t);
+            double cf;
+            int sr;
+            ldterm(p, o + 32 * t, cf, sr);
             la = fma(cf, AB[sr], la);
             lb = fma(cf, AB[NF + sr], lb);
           }
         } else {
 #pragma unroll 4
           for (int t = 0; t < c; ++t) {
-            const int sr = __ldg(p.src + o + 32 * t);
-            const double cf = __ldg(p.coef + o + 32 * t);
-            la = fma(cf, scr[2 * sr], la);
-            lb = fma(cf, scr[2 * sr + 1], lb);
+            double cf;
+            int sr;
+            ldterm(p, o + 32 * t, cf, sr);
+            const double2 v = *reinterpret_cast<const double2 *>(scr + 2 * sr);
+            la = fma(cf, v.x, la);
+            lb = fma(cf, v.y, lb);
           }
         }
-        scr[2 * d] = la;
-        scr[2 * d + 1] = lb;
+        *reinterpret_cast<double2 *>(scr + 2 * d) = make_double2(la, lb);
       }
     }
     __syncthreads();
@@ -442,7 +458,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32)
           sAB[NF + gm] = B;
         }
         __syncthreads();
-        cta_slift2<W>(pr.slift[f], sAB, N, NF, s + 3 * N, sACC, f, warp, lane);
+        cta_slift2<W>(pr.slift[f], sAB, N, NF, s + D::SCR, sACC, f, warp, lane);
       }
     }
     // S2 + S6: inverse mass with geometry, then update (X staged in slots [0,3N)) or write
@@ -473,7 +489,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32)
     }
     __syncthreads();
     if (upd && trOut)
-      for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, s, N, NF, s + 3 * N, trOut + (e * 4 + f) * 2 * NF, warp, lane);
+      for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, s, N, NF, s + D::SCR, trOut + (e * 4 + f) * 2 * NF, warp, lane);
     __syncthreads();
   }
 }
@@ -490,7 +506,7 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32) trace2_kernel(const double *_
   for (int64_t e = blockIdx.x; e < n_tet; e += gridDim.x) {
     cta_load_elem<LD, N>(X, e, cs, smem, threadIdx.x, NT);
     __syncthreads();
-    for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, smem, N, NF, smem + 3 * N, tr + (e * 4 + f) * 2 * NF, warp, lane);
+    for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, smem, N, NF, smem + D::SCR, tr + (e * 4 + f) * 2 * NF, warp, lane);
   }
 }
 
