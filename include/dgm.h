@@ -130,6 +130,16 @@ dgm_status dgm_step_host(dgm_ctx *ctx, double *E_host, double *H_host, double dt
  * two-pass reduction; writes one double to *out_host and synchronises. */
 dgm_status dgm_energy(dgm_ctx *ctx, const double *E, const double *H, double *out_host, void *cuda_stream);
 
+/* Spectral radius ρ of K = Mμ^{-1} C Mε^{-1} Cᵀ by power iteration with the
+ * Rayleigh quotient in the Mμ inner product, the operator
+ * applied through the same stage kernels as dgm_step (Ė(0,H), then Ḣ(·,0)).
+ * The symplectic-Euler step is stable for Δt ≤ 2/√ρ (reading G6: the paper's
+ * printed bound lacks the square root).  For the upwind flux K is not symmetric
+ * and ρ is an estimate.  Deterministic start vector from `seed`.  Uses internal
+ * work fields (allocated on first use) and the trace buffers, so a following
+ * dgm_step_ex(DGM_STEP_CONTINUE) recomputes them.  Synchronises each iteration. */
+dgm_status dgm_spectral_radius(dgm_ctx *ctx, int iters, uint64_t seed, double *rho_out, void *cuda_stream);
+
 /* Host copies of the integer tables, each [n_tet][4]:
  *   nbr (neighbour tet, -1 on PEC), nbr_face (its local face, -1 on PEC),
  *   sign = (-1)^f sign(det F_T), bc (0 interior incl. periodic, 1 PEC).

@@ -20,7 +20,7 @@ STATUS = {0: "DGM_OK", 1: "DGM_EINVAL", 2: "DGM_EMESH", 3: "DGM_EORDER", 4: "DGM
 FLUX = {"central": 0, "upwind": 1}
 DGM_STEP_CONTINUE = 1
 EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
-           "dgm_energy", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
+           "dgm_energy", "dgm_spectral_radius", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
 
 
 class DgmError(RuntimeError):
@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH):
         "dgm_step_ex": (I32, [P, P, P, D, I64, I32, P]),
         "dgm_step_host": (I32, [P, P, P, D, I64, P]),
         "dgm_energy": (I32, [P, P, P, P, P]),
+        "dgm_spectral_radius": (I32, [P, I32, ctypes.c_uint64, P, P]),
         "dgm_tables": (I32, [P, P, P, P, P]),
         "dgm_match_faces_host": (I32, [ctypes.POINTER(_Mesh), P, P, P, P]),
         "dgm_last_launches": (I64, [P]),
@@ -183,6 +184,20 @@ class Context:
         self._check(self._lib.dgm_energy(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
                                          ctypes.byref(out), _stream(stream)))
         return out.value
+
+    def dgm_spectral_radius(self, iters=100, seed=0, stream=None):
+        """ρ(Mμ^{-1} C Mε^{-1} Cᵀ) by power iteration; Δt_max = 2/√ρ (reading G6)."""
+        out = ctypes.c_double()
+        self._check(self._lib.dgm_spectral_radius(self.h, int(iters), ctypes.c_uint64(seed), ctypes.byref(out),
+                                                  _stream(stream)))
+        return out.value
+
+    def cfl_dt(self, iters=100, safety=0.5, seed=0):
+        """safety · 2/√ρ, rounded down to 4 significant digits (reading G6)."""
+        import math
+        dt = safety * 2.0 / math.sqrt(self.dgm_spectral_radius(iters, seed))
+        e = math.floor(math.log10(dt)) - 3
+        return math.floor(dt / 10.0 ** e) * 10.0 ** e
 
     def dgm_tables(self):
         n = self.n_tet

@@ -91,6 +91,7 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_partial);
   cudaFree(c->d_E);
   cudaFree(c->d_H);
+  for (int i = 0; i < 3; ++i) cudaFree(c->d_pw[i]);
   if (c->side) cudaStreamDestroy(c->side);
   for (int i = 0; i < 4; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
@@ -461,6 +462,50 @@ dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t 
   CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev[3], 0));
   CUDA_TRY(c, cudaStreamSynchronize(st));
   c->tr_valid = false;   // the caller owns the host copies now
+  return DGM_OK;
+}
+
+dgm_status dgm_spectral_radius(dgm_ctx *c, int iters, uint64_t seed, double *rho_out, void *stream) {
+  if (!c || !rho_out || iters < 1) return dgm::set_err(c, DGM_EINVAL, "bad spectral_radius arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * 3 * (size_t)c->n_tet * c->LD;
+  for (int i = 0; i < 3; ++i)
+    if (!c->d_pw[i]) {
+      CUDA_TRY(c, cudaMalloc(&c->d_pw[i], bytes));
+      CUDA_TRY(c, cudaMemsetAsync(c->d_pw[i], 0, bytes, st));
+    }
+  double *Hv = c->d_pw[0], *D = c->d_pw[1], *W = c->d_pw[2];
+  c->tr_valid = false;   // the trace buffers are used as scratch here
+  dgm_status r = dgm::launch_seed(c, Hv, seed, st);
+  // zero field for the "other" argument (E = 0 for Ė(0, H); H = 0 for Ḣ(D, 0))
+  double *Z = W;
+  double rho = 0.0;
+  for (int it = 0; it < iters && r == DGM_OK; ++it) {
+    double nrm2 = 0.0;
+    if ((r = dgm::launch_massdot(c, Hv, Hv, 1, &nrm2, st)) != DGM_OK) break;
+    if (!(nrm2 > 0.0) || !std::isfinite(nrm2)) return dgm::set_err(c, DGM_EINVAL, "power iteration broke down");
+    if ((r = dgm::launch_scale(c, Hv, Hv, 1.0 / std::sqrt(nrm2), st)) != DGM_OK) break;
+    // D = Ė(0, H) = -Mε^{-1} Cᵀ H   (curl + face parts; upwind E-terms vanish for E = 0)
+    CUDA_TRY(c, cudaMemsetAsync(Z, 0, bytes, st));
+    if ((r = dgm::launch_tb_traces(c, Hv, c->d_tr[2], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[0], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_stage(c, dgm::STAGE_E, Hv, nullptr, D, 0.0, 1, 1, dgm::OUT_WRITE, c->d_tr[2], c->d_tr[0],
+                                  nullptr, st)) != DGM_OK)
+      break;
+    // W = Ḣ(D, 0) = Mμ^{-1} C D
+    if ((r = dgm::launch_tb_traces(c, D, c->d_tr[0], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[2], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_stage(c, dgm::STAGE_H, D, nullptr, W, 0.0, 1, 1, dgm::OUT_WRITE, c->d_tr[0], c->d_tr[2],
+                                  nullptr, st)) != DGM_OK)
+      break;
+    // K H = -W;  Rayleigh quotient ρ = (H, Mμ K H) with ‖H‖_Mμ = 1
+    double hw = 0.0;
+    if ((r = dgm::launch_massdot(c, Hv, W, 1, &hw, st)) != DGM_OK) break;
+    rho = -hw;
+    if ((r = dgm::launch_scale(c, Hv, W, -1.0, st)) != DGM_OK) break;
+  }
+  if (r != DGM_OK) return r;
+  *rho_out = rho;
   return DGM_OK;
 }
 

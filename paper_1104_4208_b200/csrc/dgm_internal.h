@@ -107,6 +107,7 @@ struct dgm_ctx {
   double *d_partial = nullptr; // energy partial sums
   int64_t n_partial = 0;
   double *d_E = nullptr, *d_H = nullptr;   // device copies for dgm_step_host
+  double *d_pw[3] = {nullptr, nullptr, nullptr};   // power-iteration work fields
   cudaStream_t side = nullptr;             // dgm_step_host: H copies overlap the kernels
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
@@ -127,6 +128,9 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
 dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
 int workspace_doubles(int p);
+dgm_status launch_massdot(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out, cudaStream_t st);
+dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaStream_t st);
+dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
 // lane-per-element path (dgm_lane.cu), p <= kLanePmax
 constexpr int kLanePmax = 6;
 dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,

@@ -661,6 +661,102 @@ dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_
   DGM_DISPATCH_HI(c->p, launch_trace2_p, c, X, tr, st)
 }
 
+// (A, M_m B) = Σ_T |det F| m_T Σ_α ‖φ_α‖² A_αᵀ F^{-1}F^{-T} B_α  (m = ε or μ), the
+// mass inner product of the covariant fields; per-block partials.
+template <int P>
+__global__ void massdot_kernel(const double *__restrict__ A, const double *__restrict__ B, const Geo *__restrict__ geo,
+                               const double *__restrict__ norms, int64_t n_tet, int use_mu, double *partial) {
+  using D = Dim<P>;
+  constexpr int N = D::N, LD = D::LD;
+  const int64_t cstride = n_tet * LD;
+  double sum = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_tet; e += (int64_t)gridDim.x * blockDim.x) {
+    const Geo g = geo[e];
+    const double a = g.g[0], b = g.g[1], c = g.g[2], d = g.g[3], f = g.g[4], h = g.g[5];
+    const double c00 = d * h - f * f, c01 = c * f - b * h, c02 = b * f - c * d;
+    const double c11 = a * h - c * c, c12 = b * c - a * f, c22 = a * d - b * b;
+    const double det = a * c00 + b * c01 + c * c02;
+    const double m = use_mu ? 1.0 / g.inv_mu : 1.0 / g.inv_eps;
+    double se = 0.0;
+    for (int al = 0; al < N; ++al) {
+      const int64_t o = e * LD + al;
+      const double a0 = A[o], a1 = A[cstride + o], a2 = A[2 * cstride + o];
+      const double b0 = B[o], b1 = B[cstride + o], b2 = B[2 * cstride + o];
+      const double q = c00 * a0 * b0 + c11 * a1 * b1 + c22 * a2 * b2 + c01 * (a0 * b1 + a1 * b0) +
+                       c02 * (a0 * b2 + a2 * b0) + c12 * (a1 * b2 + a2 * b1);
+      se += norms[al] * q;
+    }
+    const double sg = g.detF > 0 ? 1.0 : -1.0;
+    sum += sg / det * m * se;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// X[:, :, :N] = s * Y[:, :, :N] (padding untouched; X == Y allowed)
+__global__ void scale_kernel(double *X, const double *Y, double s, int64_t n_tet, int N, int LD) {
+  const int64_t total = 3 * n_tet * LD;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    if (i % LD < N) X[i] = s * Y[i];
+}
+
+// deterministic start vector for the power iteration: a counter-based hash of the
+// index mapped to [-1, 1) (splitmix64), modes damped by 1/(1+mode)
+__global__ void seed_kernel(double *X, uint64_t seed, int64_t n_tet, int N, int LD) {
+  const int64_t total = 3 * n_tet * LD;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int al = (int)(i % LD);
+    if (al >= N) { X[i] = 0.0; continue; }
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    X[i] = ((double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0) / (1.0 + al);
+  }
+}
+
+template <int P>
+static dgm_status launch_massdot_p(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out,
+                                   cudaStream_t st) {
+  const int threads = 256;
+  int64_t grid = (c->n_tet + threads - 1) / threads;
+  if (grid > 4 * (int64_t)c->sms) grid = 4 * (int64_t)c->sms;
+  if (c->n_partial < grid + 1) {
+    cudaFree(c->d_partial);
+    if (cudaMalloc(&c->d_partial, sizeof(double) * (grid + 1)) != cudaSuccess)
+      return set_err(c, DGM_ENOMEM, "partials");
+    c->n_partial = grid + 1;
+  }
+  massdot_kernel<P><<<(unsigned)grid, threads, 0, st>>>(A, B, c->d_geo, c->progs.norms, c->n_tet, use_mu, c->d_partial);
+  sum_kernel<<<1, 256, 0, st>>>(c->d_partial, (int)grid, c->d_partial + grid);
+  cudaError_t e = cudaMemcpyAsync(out, c->d_partial + grid, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("massdot: ") + cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+dgm_status launch_massdot(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out, cudaStream_t st) {
+  DGM_DISPATCH(c->p, launch_massdot_p, c, A, B, use_mu, out, st)
+}
+
+dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaStream_t st) {
+  scale_kernel<<<4 * c->sms, 256, 0, st>>>(X, Y, s, c->n_tet, c->N, c->LD);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("scale: ") + cudaGetErrorString(e));
+}
+
+dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st) {
+  seed_kernel<<<4 * c->sms, 256, 0, st>>>(X, seed, c->n_tet, c->N, c->LD);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("seed: ") + cudaGetErrorString(e));
+}
+
 template <int P>
 static dgm_status launch_energy_p(dgm_ctx *c, const double *E, const double *H, double *out, cudaStream_t st) {
   const int threads = 256;

@@ -235,3 +235,36 @@ def test_step_host_matches_device_step(case, p):
     c.dgm_step_host(Eh, Hh, 1e-3, 1)
     c.dgm_step(Ed, Hd, 1e-3, 1)
     assert torch.equal(Eh, Ed.cpu()) and torch.equal(Hh, Hd.cpu())
+
+
+def test_spectral_radius_vs_dense_eigen():
+    """NEXT-3: the GPU power iteration finds the largest
+    eigenvalue of K = Mμ^{-1} C Mε^{-1} Cᵀ, checked against a dense eigensolve of
+    the tier-A matrices, and Δt = 2/√ρ is the stability boundary (reading G6)."""
+    p = 2
+    m, rep, eps, mu = _problem(2, (False,) * 3, p, "central")
+    A = TierA(m.xyz, m.tet, rep, p, eps, mu)
+    o = A.ops
+    n, nd = m.n_tet, 3 * A.N
+    import scipy.linalg as sl
+    Meps = sl.block_diag(*o["Meps"])
+    Mmu = sl.block_diag(*o["Mmu"])
+    C = (o["HE_vol"] + o["HE_face"]).toarray()
+    EH = (o["EH_vol"] + o["EH_face"]).toarray()     # = -Cᵀ
+    K = -np.linalg.solve(Mmu, C @ np.linalg.solve(Meps, EH))
+    lam = np.max(np.abs(np.linalg.eigvals(K)))
+    c = _ctx(m, rep, p, eps, mu, "central")
+    rho = c.dgm_spectral_radius(400, seed=3)
+    assert rho == pytest.approx(lam, rel=2e-3)
+    # the symplectic-Euler stability boundary
+    rng = np.random.default_rng(0)
+    E = rng.standard_normal((3, n, c.N))
+    H = rng.standard_normal((3, n, c.N))
+    dtmax = 2.0 / np.sqrt(lam)
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    w0 = c.dgm_energy(Ed, Hd)
+    c.dgm_step(Ed, Hd, 0.95 * dtmax, 400)
+    assert c.dgm_energy(Ed, Hd) < 100 * w0
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    c.dgm_step(Ed, Hd, 1.2 * dtmax, 400)
+    assert not (c.dgm_energy(Ed, Hd) < 1e6 * w0)
