@@ -127,7 +127,6 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
                            cudaStream_t st);
 dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
-int workspace_doubles(int p);
 dgm_status launch_massdot(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out, cudaStream_t st);
 dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaStream_t st);
 dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);

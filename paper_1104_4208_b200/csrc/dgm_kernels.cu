@@ -1,17 +1,18 @@
-// DG Maxwell stage kernels for sm_100a (FP64).
+// High-order (p > kLanePmax) stage kernels for sm_100a (FP64), the trace-buffer
+// launchers for all orders, and the reductions (energy, mass inner product).
 //
-// One warp owns one element at a time (grid-stride over elements); the
-// element's workspace lives in shared memory.  Per element a stage does
-// (DESIGN.md "Kernels"):
-//   S1  reference curl of the source field Ŷ by the sparse recurrence sweeps
-//       (level-scheduled pull-form program from gen/plan.py)
-//   S3  tangential traces a_k = Ŷ·t̂_k on the 4 faces, own element and the
-//       neighbour's copy of each face (exact restriction)
+// A CTA of W warps owns one element at a time (grid-stride); its workspace lives
+// in shared memory.  Per element a stage does:
+//   S1  reference curl of Ŷ by the sparse recurrence sweeps (level-scheduled
+//       pull-form program from gen/plan.py)
+//   S3  own and neighbour tangential traces of Ŷ read from the trace buffer
 //   S4  numerical flux on the face modes (central or upwind, PEC mirror)
-//   S5  lift back to volume modes (traceᵀ with ‖ψ‖²/‖φ‖² folded in)
+//   S5  lift back to volume modes (sum-factorised staged transpose of the trace,
+//       ‖ψ‖²/‖φ‖² folded in)
 //   S2  inverse mass + geometry: Ẋ_β = ±(1/m_T) G'_T (ĉ_β + L_β),
 //       G'_T = F_TᵀF_T/det F_T (covariant identities :367-370)
-//   S6  update X += dt Ẋ (symplectic Euler) or write Ẋ.
+//   S6  update X += dt Ẋ (symplectic Euler) or write Ẋ, then
+//       the traces of the updated field for the next stage.
 #include <cstdint>
 #include <cstdio>
 
@@ -19,17 +20,12 @@
 
 namespace dgm {
 
+// mode counts of order P (graded Dubiner basis, SURVEY.md §8 notation)
 template <int P>
 struct Dim {
   static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
   static constexpr int NF = (P + 1) * (P + 2) / 2;
   static constexpr int LD = (N + 3) & ~3;
-  static constexpr int ACC = 9 * N;                 // must match gen/plan.py
-  static constexpr int FLUXSZ = 8 * NF + 3 * N + 2 * NF + 3 * NF;
-  static constexpr int FLUX_BASE = (FLUXSZ <= 6 * N) ? 3 * N : 12 * N;
-  static constexpr int WS = (FLUX_BASE + FLUXSZ > 12 * N) ? FLUX_BASE + FLUXSZ : 12 * N;
-  static constexpr int WARPS_RAW = (96 * 1024) / (WS * 8);
-  static constexpr int WARPS = WARPS_RAW < 1 ? 1 : (WARPS_RAW > 8 ? 8 : WARPS_RAW);
 };
 
 // warp path with trace buffers: slots [0,9N) sweep (Ŷ then u), acc at 9N, A/B at 12N
@@ -68,87 +64,6 @@ __device__ __forceinline__ void tangential(const double *sY, int N, int a, doubl
   }
 }
 
-// Generic level-scheduled program: s[dst] = Σ coef * s[src]
-__device__ __forceinline__ void run_assign(const DevProg &p, double *s, int lane) {
-  for (int ps = 0; ps < p.npass; ++ps) {
-    const int row = ps * 32 + lane;
-    const unsigned d = __ldg(p.dst + row);
-    if (d != 0xFFFFu) {
-      const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + ps) * 32 + lane;
-      double acc = 0.0;
-      for (int t = 0; t < c; ++t) acc = fma(__ldg(p.coef + o + 32 * t), s[__ldg(p.src + o + 32 * t)], acc);
-      s[d] = acc;
-    }
-    if (__ldg(p.sync + ps)) __syncwarp();
-  }
-}
-
-// Face-F tangential traces of the volume field sY -> out[0..NF) (k=1), out[NF..2NF) (k=2)
-template <int F>
-__device__ __forceinline__ void run_trace_f(const DevProg &p, const double *sY, int N, int NF, double *out, int lane) {
-  for (int ps = 0; ps < p.npass; ++ps) {
-    const int row = ps * 32 + lane;
-    const unsigned g = __ldg(p.dst + row);
-    if (g != 0xFFFFu) {
-      const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + ps) * 32 + lane;
-      double t1 = 0.0, t2 = 0.0;
-      for (int t = 0; t < c; ++t) {
-        double a1, a2;
-        tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
-        const double cf = __ldg(p.coef + o + 32 * t);
-        t1 = fma(cf, a1, t1);
-        t2 = fma(cf, a2, t2);
-      }
-      out[g] = t1;
-      out[NF + g] = t2;
-    }
-  }
-}
-
-__device__ __forceinline__ void run_trace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *out,
-                                          int lane) {
-  switch (f) {
-    case 0: run_trace_f<0>(pr.trace[0], sY, N, NF, out, lane); break;
-    case 1: run_trace_f<1>(pr.trace[1], sY, N, NF, out, lane); break;
-    case 2: run_trace_f<2>(pr.trace[2], sY, N, NF, out, lane); break;
-    default: run_trace_f<3>(pr.trace[3], sY, N, NF, out, lane); break;
-  }
-}
-
-// acc[m][β] += Σ_γ L_f[β,γ] q[m][γ]
-__device__ __forceinline__ void run_lift(const DevProg &p, const double *q, int N, int NF, double *acc, int lane) {
-  for (int ps = 0; ps < p.npass; ++ps) {
-    const int row = ps * 32 + lane;
-    const unsigned b = __ldg(p.dst + row);
-    if (b != 0xFFFFu) {
-      const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + ps) * 32 + lane;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      for (int t = 0; t < c; ++t) {
-        const int g = __ldg(p.src + o + 32 * t);
-        const double cf = __ldg(p.coef + o + 32 * t);
-        a0 = fma(cf, q[g], a0);
-        a1 = fma(cf, q[NF + g], a1);
-        a2 = fma(cf, q[2 * NF + g], a2);
-      }
-      acc[b] += a0;
-      acc[N + b] += a1;
-      acc[2 * N + b] += a2;
-    }
-  }
-}
-
-template <int LDv, int Nv>
-__device__ __forceinline__ void load_elem(const double *__restrict__ F, int64_t e, int64_t cstride, double *s,
-                                          int lane) {
-  for (int c = 0; c < 3; ++c) {
-    const double *src = F + c * cstride + e * LDv;
-    for (int i = lane; i < Nv; i += 32) s[c * Nv + i] = __ldg(src + i);
-  }
-}
-
 __device__ __forceinline__ void ldterm(const DevProg &p, int q, double &cf, int &src) {
   const double2 v = __ldg(p.term + q);
   cf = v.x;
@@ -183,68 +98,6 @@ __device__ __forceinline__ void cta_assign(const DevProg &p, double *s, int warp
     }
     __syncthreads();
     ps = pe + 1;
-  }
-}
-
-template <int F, int W>
-__device__ __forceinline__ void cta_trace_f(const DevProg &p, const double *sY, int N, int NF, double *out, int warp,
-                                            int lane) {
-  for (int q = warp; q < p.npass; q += W) {
-    const int row = q * 32 + lane;
-    const unsigned g = __ldg(p.dst + row);
-    if (g != 0xFFFFu) {
-      const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + q) * 32 + lane;
-      double t1 = 0.0, t2 = 0.0;
-#pragma unroll 4
-      for (int t = 0; t < c; ++t) {
-        double a1, a2;
-        tangential<F>(sY, N, __ldg(p.src + o + 32 * t), a1, a2);
-        const double cf = __ldg(p.coef + o + 32 * t);
-        t1 = fma(cf, a1, t1);
-        t2 = fma(cf, a2, t2);
-      }
-      out[g] = t1;
-      out[NF + g] = t2;
-    }
-  }
-}
-
-template <int W>
-__device__ __forceinline__ void cta_trace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *out,
-                                          int warp, int lane) {
-  switch (f) {
-    case 0: cta_trace_f<0, W>(pr.trace[0], sY, N, NF, out, warp, lane); break;
-    case 1: cta_trace_f<1, W>(pr.trace[1], sY, N, NF, out, warp, lane); break;
-    case 2: cta_trace_f<2, W>(pr.trace[2], sY, N, NF, out, warp, lane); break;
-    default: cta_trace_f<3, W>(pr.trace[3], sY, N, NF, out, warp, lane); break;
-  }
-}
-
-// acc[m][β] += t̂1_m Σ_γ L_f[β,γ] A_γ + t̂2_m Σ_γ L_f[β,γ] B_γ  (rows split over the W warps)
-template <int W>
-__device__ __forceinline__ void cta_lift2(const DevProg &p, const double *AB, int N, int NF, double *acc, int f,
-                                          int warp, int lane) {
-  const double a0 = kT1[f][0], a1 = kT1[f][1], a2 = kT1[f][2];
-  const double b0 = kT2[f][0], b1 = kT2[f][1], b2 = kT2[f][2];
-  for (int q = warp; q < p.npass; q += W) {
-    const int row = q * 32 + lane;
-    const unsigned b = __ldg(p.dst + row);
-    if (b != 0xFFFFu) {
-      const int c = __ldg(p.cnt + row);
-      const int o = __ldg(p.off + q) * 32 + lane;
-      double la = 0.0, lb = 0.0;
-#pragma unroll 4
-      for (int t = 0; t < c; ++t) {
-        const int g = __ldg(p.src + o + 32 * t);
-        const double cf = __ldg(p.coef + o + 32 * t);
-        la = fma(cf, AB[g], la);
-        lb = fma(cf, AB[NF + g], lb);
-      }
-      acc[b] += a0 * la + b0 * lb;
-      acc[N + b] += a1 * la + b1 * lb;
-      acc[2 * N + b] += a2 * la + b2 * lb;
-    }
   }
 }
 
@@ -780,20 +633,5 @@ dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *o
   DGM_DISPATCH(c->p, launch_energy_p, c, E, H, out, st)
 }
 
-int workspace_doubles(int p) {
-  switch (p) {
-    case 1: return Dim<1>::WS;
-    case 2: return Dim<2>::WS;
-    case 3: return Dim<3>::WS;
-    case 4: return Dim<4>::WS;
-    case 5: return Dim<5>::WS;
-    case 6: return Dim<6>::WS;
-    case 7: return Dim<7>::WS;
-    case 8: return Dim<8>::WS;
-    case 9: return Dim<9>::WS;
-    case 10: return Dim<10>::WS;
-  }
-  return 0;
-}
 
 }  // namespace dgm
