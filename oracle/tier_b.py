@@ -268,3 +268,93 @@ class _SubView:
 
     _lift_cross = TierB._lift_cross
     _lift_tan = TierB._lift_tan
+
+
+class TierBStab(TierB):
+    """Stabilised central flux with face unknowns H^F (NEXT-1).
+
+    Face unknown H^F on each face F: a tangential field of degree p, stored by its
+    covariant components H_k = H^F·t_k (k = 1, 2; t_k the physical edge vectors
+    of the face's vertex-ordered frame, reading G9) in the face basis ψ_γ.
+    With ν_T the outward normal of T and σ_{T,f} = (-1)^f sgn(det F_T) (App. A.6)
+    the system (signs: reading G1/G16) is
+      (εĖ, e)_T      = central E-eq  - Σ_f σ_{T,f} ∫ (H^F_1 e_2 - H^F_2 e_1) du dv
+      (μḢ, h)_T      = central H-eq
+      (α/h_F) ∫ Ḣ^F·h^F ds = Σ_{T∋F} σ_{T,f} ∫ (E_2 h_1 - E_1 h_2) du dv
+    i.e. Σ_F (H^F×ν, [[e]])_F in the E equation and ([[E]]×ν, h^F)_F in the face
+    equation with the same sign, which makes the semi-discrete system skew, so
+    ½(εE,E) + ½(μH,H) + ½Σ_F(α/h_F)(H^F,H^F)_F is conserved.
+    On a PEC face [[E]] = E⁻ (one side).  Readings: α = alpha0·p²,
+    h_F = sqrt(|t₁×t₂|) (G16).  Per face mode γ the face mass is (α/h_F) M ‖ψ_γ‖²
+    with M = |t₁×t₂| g⁻¹ (as for the upwind flux)."""
+
+    def __init__(self, xyz, tet, rep, p, eps, mu, alpha0=1.0):
+        super().__init__(xyz, tet, rep, p, eps, mu, "central")
+        n = self.n_tet
+        # face numbering: each interior face once (owned by the smaller tet), PEC faces once
+        fid = -np.ones((n, 4), dtype=np.int64)
+        owner = []
+        for T in range(n):
+            for f in range(4):
+                S = self.nbr[T, f]
+                if self.pec[T, f] or T < S:
+                    fid[T, f] = len(owner)
+                    owner.append((T, f))
+        for T in range(n):
+            for f in range(4):
+                if fid[T, f] < 0:
+                    fid[T, f] = fid[self.nbr[T, f], self.nbr_face[T, f]]
+        self.fid = fid
+        self.n_faces = len(owner)
+        self.owner = np.array(owner)
+        ot, of = self.owner[:, 0], self.owner[:, 1]
+        t = np.einsum("tmj,fkj->tfkm", self.F, self.that)[ot, of]             # [nF, 2, 3] physical t_k
+        area = np.linalg.norm(np.cross(t[:, 0], t[:, 1]), axis=-1)
+        self.hF = np.sqrt(area)
+        self.alpha = alpha0 * p * p
+        self.Mf = self.M[ot, of]                                               # [nF, 2, 2]
+
+    def _lift_HF(self, HF):
+        """-Σ_f (-1)^f Λ_f(H^F) in the dE accumulator frame (before 1/‖φ‖², G')."""
+        D = HF[self.fid]                                                       # [n, 4, 2, NF]
+        return -self._lift_cross(D)
+
+    def dE(self, E, H, HF=None, part="all"):
+        out = super().dE(E, H, part)
+        if HF is not None and part in ("all", "flux"):
+            R = self._lift_HF(HF) / self.R["norms"][None, None, :]
+            out = out + self._apply_G(R, 1.0 / self.eps)
+        return out
+
+    def dHF(self, E):
+        """Ḣ^F_γ = (h_F/α) M⁻¹ Σ_{T∋F} σ_{T,f} (E_2, -E_1)_γ."""
+        trE = self.traces(E)                                                   # [n,4,2,NF]
+        NF = trE.shape[-1]
+        rhs = np.zeros((self.n_faces, 2, NF))
+        for T in range(self.n_tet):
+            for f in range(4):
+                s = float(self.sign[T, f])
+                k = self.fid[T, f]
+                rhs[k, 0] += s * trE[T, f, 1]
+                rhs[k, 1] -= s * trE[T, f, 0]
+        Minv = np.linalg.inv(self.Mf)
+        return (self.hF / self.alpha)[:, None, None] * np.einsum("fkl,flg->fkg", Minv, rhs)
+
+    def energy(self, E, H, HF=None):
+        w = super().energy(E, H)
+        if HF is not None:
+            fn = self.R["fnorms"]
+            q = np.einsum("fkg,fkl,flg->fg", HF, self.Mf, HF) @ fn
+            w += 0.5 * float(np.sum(self.alpha / self.hF * q))
+        return w
+
+
+def symplectic_euler_stab(B, E, H, HF, dt, nsteps):
+    """H, H^F ← H, H^F + dt (Ḣ, Ḣ^F)(E);  E ← E + dt Ė(H, H^F)  (PAPER.md:277-280
+    with the magnetic unknowns extended by H^F)."""
+    E, H, HF = (np.array(x, dtype=np.float64, copy=True) for x in (E, H, HF))
+    for _ in range(nsteps):
+        dH, dHF = B.dH(E, H), B.dHF(E)
+        H, HF = H + dt * dH, HF + dt * dHF
+        E = E + dt * B.dE(E, H, HF)
+    return E, H, HF

@@ -1,0 +1,88 @@
+"""Pins of the oracle's stabilised central flux with face unknowns H^F
+(NEXT-1).  CPU only."""
+import itertools
+
+import numpy as np
+import pytest
+
+import dgm_inputs as di
+from oracle.tier_a import TierA, to_global
+from oracle.tier_b import TierBStab, symplectic_euler_stab
+
+
+def _mesh(n, periodic, seed=4):
+    m = di.kuhn_mesh(n, periodic=periodic, jitter=0.1, seed=seed)
+    return m, (m.rep if any(periodic) else None)
+
+
+@pytest.mark.parametrize("periodic,n", [((False,) * 3, 2), ((True,) * 3, 3), ((False, True, True), 3)])
+def test_stab_energy_conserved_semi_discrete(periodic, n):
+    """with H^F the system stays skew, so
+    d/dt[½(εE,E) + ½(μH,H) + ½Σ_F(α/h)(H^F,H^F)] = 0."""
+    m, rep = _mesh(n, periodic)
+    rng = np.random.default_rng(0)
+    eps, mu = rng.uniform(1, 4, m.n_tet), rng.uniform(1, 2, m.n_tet)
+    p = 2
+    B = TierBStab(m.xyz, m.tet, rep, p, eps, mu)
+    A = TierA(m.xyz, m.tet, rep, p, eps, mu)
+    E = rng.standard_normal((3, m.n_tet, B.N))
+    H = rng.standard_normal((3, m.n_tet, B.N))
+    HF = rng.standard_normal((B.n_faces, 2, 6))
+    dE, dH, dHF = B.dE(E, H, HF), B.dH(E, H), B.dHF(E)
+    nd = 3 * B.N
+    w = sum(to_global(E).reshape(-1, nd)[T] @ A.ops["Meps"][T] @ to_global(dE).reshape(-1, nd)[T]
+            + to_global(H).reshape(-1, nd)[T] @ A.ops["Mmu"][T] @ to_global(dH).reshape(-1, nd)[T]
+            for T in range(m.n_tet))
+    w += float(np.sum(B.alpha / B.hF * (np.einsum("fkg,fkl,flg->fg", HF, B.Mf, dHF) @ B.R["fnorms"])))
+    scale = np.sqrt(B.energy(E, H, HF) * B.energy(dE, dH, dHF))
+    assert abs(w) <= 1e-12 * scale
+
+
+def _interior_lagrange_dofs(m, q):
+    """Interior DOFs of continuous P^q Lagrange on a PEC unit-cube mesh."""
+    X, T = m.xyz, m.tet
+    on_plane = lambda vs: any(all(np.isclose(X[v][a], c) for v in vs) for a in range(3) for c in (0.0, 1.0))
+    verts = set(T.ravel().tolist())
+    edges = {tuple(sorted(e)) for t in T for e in itertools.combinations(t, 2)}
+    faces = {tuple(sorted(f)) for t in T for f in itertools.combinations(t, 3)}
+    Vi = sum(1 for v in verts if not on_plane([v]))
+    Ei = sum(1 for e in edges if not on_plane(e))
+    Fi = sum(1 for f in faces if not on_plane(f))
+    return Vi + Ei * (q - 1) + Fi * (q - 1) * (q - 2) // 2 + len(T) * (q - 1) * (q - 2) * (q - 3) // 6
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_stabilisation_removes_spurious_modes(p):
+    """the kernel of the stabilised second-order
+    operator on E is exactly the discrete gradients — the interior DOFs of
+    continuous P^{p+1} Lagrange — while the plain central flux has spurious
+    near-zero modes in addition."""
+    m, rep = _mesh(2, (False,) * 3)
+    B = TierBStab(m.xyz, m.tet, rep, p, 1.0, 1.0)
+    n, N, NF = m.n_tet, B.N, (p + 1) * (p + 2) // 2
+    nE, nHF = 3 * n * N, B.n_faces * 2 * NF
+    zE = np.zeros((3, n, N))
+    zF = np.zeros((B.n_faces, 2, NF))
+    unit = lambda k, j: np.eye(1, k, j).ravel()
+    CH = np.array([B.dH(unit(nE, j).reshape(3, n, N), zE).ravel() for j in range(nE)]).T
+    CF = np.array([B.dHF(unit(nE, j).reshape(3, n, N)).ravel() for j in range(nE)]).T
+    EH = np.array([B.dE(zE, unit(nE, j).reshape(3, n, N), zF).ravel() for j in range(nE)]).T
+    EF = np.array([B.dE(zE, zE, unit(nHF, j).reshape(B.n_faces, 2, NF)).ravel() for j in range(nHF)]).T
+    count = lambda K: int(np.sum((ev := np.abs(np.linalg.eigvals(K))) < 1e-9 * ev.max()))
+    ks = count(-(EH @ CH + EF @ CF))
+    kc = count(-(EH @ CH))
+    assert ks == _interior_lagrange_dofs(m, p + 1)
+    assert kc > ks
+
+
+def test_stab_leapfrog_energy_bounded():
+    m, rep = _mesh(2, (False,) * 3)
+    p = 2
+    B = TierBStab(m.xyz, m.tet, rep, p, 1.0, 1.0)
+    rng = np.random.default_rng(2)
+    E = rng.standard_normal((3, m.n_tet, B.N))
+    H = np.zeros_like(E)
+    HF = np.zeros((B.n_faces, 2, 6))
+    w0 = B.energy(E, H, HF)
+    E1, H1, HF1 = symplectic_euler_stab(B, E, H, HF, 1e-3, 100)
+    assert B.energy(E1, H1, HF1) == pytest.approx(w0, rel=0.05)
