@@ -62,8 +62,11 @@ typedef enum {
 #define DGM_PMAX 10
 
 typedef enum {
-  DGM_FLUX_CENTRAL = 0, /* H* = {{H}}, E* = {{E}} */
-  DGM_FLUX_UPWIND = 1   /* Riemann flux, Z = sqrt(μ/ε)               (reading G2)       */
+  DGM_FLUX_CENTRAL = 0,    /* H* = {{H}}, E* = {{E}} */
+  DGM_FLUX_UPWIND = 1,     /* Riemann flux, Z = sqrt(μ/ε)               (reading G2)       */
+  DGM_FLUX_STABILIZED = 2  /* central flux + face unknowns H^F with face mass (α/h_F):
+                              energy-conserving and free of spurious modes
+                              (readings G16-G17); use the *_sc calls */
 } dgm_flux;
 
 typedef struct {
@@ -78,6 +81,7 @@ typedef struct {
   int32_t flux;          /* dgm_flux                                          */
   int32_t eps_per_elem;  /* 0: eps points to one double; 1: to [n_tet]        */
   int32_t mu_per_elem;   /* same for mu                                       */
+  double alpha0;         /* DGM_FLUX_STABILIZED: α = alpha0·p² (≤0 → 1)       */
 } dgm_opts;
 
 /* Validate the mesh, match faces, compute per-element geometry
@@ -106,7 +110,10 @@ dgm_status dgm_apply_flux(dgm_ctx *ctx, const double *E, const double *H, double
 /* nsteps of the symplectic-Euler map (reading G7: H staggered)
  *   H ← H + dt Ḣ(E, H);   E ← E + dt Ė(H, E)
  * in place on the device arrays E, H.  Upwind self-terms use the current value
- * of the field being updated. */
+ * of the field being updated.  DGM_EINVAL for a DGM_FLUX_STABILIZED context
+ * (its state includes H^F: use dgm_step_sc); the same holds for dgm_step_ex and
+ * dgm_step_host.  dgm_apply_flux and dgm_spectral_radius on such a context act
+ * with the central flux alone (H^F = 0). */
 dgm_status dgm_step(dgm_ctx *ctx, double *E, double *H, double dt, int64_t nsteps, void *cuda_stream);
 
 /* Flags for dgm_step_ex. */
@@ -129,6 +136,37 @@ dgm_status dgm_step_host(dgm_ctx *ctx, double *E_host, double *H_host, double dt
 /* Discrete energy ½(E,MεE) + ½(H,MμH), deterministic
  * two-pass reduction; writes one double to *out_host and synchronises. */
 dgm_status dgm_energy(dgm_ctx *ctx, const double *E, const double *H, double *out_host, void *cuda_stream);
+
+/* ---- stabilised central flux (DGM_FLUX_STABILIZED) ----------
+ * Face unknowns: HF is a device array double[n_faces][2][N_F], per face the
+ * covariant tangential components H^F·t_k (k = 1, 2; t_k the physical edges of
+ * the face's ascending-vertex frame) in the face Dubiner basis ψ_γ (graded
+ * order).  Faces are numbered by scanning (tet, local face) in ascending order
+ * and counting a face at its first tet (interior faces: the smaller tet; PEC
+ * faces: their only tet).  With ν_F the outward normal of that tet and
+ * [[e]] = e⁻ − e⁺ the system (central part per reading G1) is
+ *   (εĖ,e)    = central E-eq + Σ_F (H^F×ν_F, [[e]])_F
+ *   (μḢ,h)_T  = central H-eq
+ *   (α/h_F)(Ḣ^F, h^F)_F = ([[E]]×ν, h^F)_F       (PEC faces: [[E]] = E⁻)
+ * with α = alpha0·p², h_F = sqrt(|t₁×t₂|).  It conserves
+ * ½(εE,E) + ½(μH,H) + ½Σ_F (α/h_F)(H^F,H^F)_F. */
+
+/* n_faces and, if face_id != NULL, the face index of every [n_tet][4] slot
+ * (host int32).  DGM_EINVAL unless the context is DGM_FLUX_STABILIZED. */
+dgm_status dgm_faces(const dgm_ctx *ctx, int64_t *n_faces, int32_t *face_id);
+
+/* nsteps of symplectic Euler with the magnetic unknowns (H, H^F) advanced
+ * together: (H, HF) += dt (Ḣ, Ḣ^F)(E);  E += dt Ė(H, HF).  flags as dgm_step_ex. */
+dgm_status dgm_step_sc(dgm_ctx *ctx, double *E, double *H, double *HF, double dt, int64_t nsteps, int flags,
+                       void *cuda_stream);
+
+/* Full time derivatives (volume + faces) of the stabilised system; NULL outputs skip. */
+dgm_status dgm_rhs_sc(dgm_ctx *ctx, const double *E, const double *H, const double *HF, double *dE, double *dH,
+                      double *dHF, void *cuda_stream);
+
+/* ½(E,MεE) + ½(H,MμH) + ½Σ_F(α/h_F)(H^F,H^F)_F; synchronises. */
+dgm_status dgm_energy_sc(dgm_ctx *ctx, const double *E, const double *H, const double *HF, double *out_host,
+                         void *cuda_stream);
 
 /* Spectral radius ρ of K = Mμ^{-1} C Mε^{-1} Cᵀ by power iteration with the
  * Rayleigh quotient in the Mμ inner product, the operator

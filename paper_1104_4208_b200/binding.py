@@ -17,10 +17,10 @@ LIB_PATH = os.path.join(HERE, "libdgm.so")
 
 DGM_OK, DGM_EINVAL, DGM_EMESH, DGM_EORDER, DGM_ECUDA, DGM_ENOMEM = range(6)
 STATUS = {0: "DGM_OK", 1: "DGM_EINVAL", 2: "DGM_EMESH", 3: "DGM_EORDER", 4: "DGM_ECUDA", 5: "DGM_ENOMEM"}
-FLUX = {"central": 0, "upwind": 1}
+FLUX = {"central": 0, "upwind": 1, "stabilized": 2}
 DGM_STEP_CONTINUE = 1
 EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
-           "dgm_energy", "dgm_spectral_radius", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
+           "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
 
 
 class DgmError(RuntimeError):
@@ -35,7 +35,8 @@ class _Mesh(ctypes.Structure):
 
 
 class _Opts(ctypes.Structure):
-    _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32)]
+    _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32),
+                ("alpha0", ctypes.c_double)]
 
 
 _lib = None
@@ -60,6 +61,10 @@ def load_library(path: str = LIB_PATH):
         "dgm_step_host": (I32, [P, P, P, D, I64, P]),
         "dgm_energy": (I32, [P, P, P, P, P]),
         "dgm_spectral_radius": (I32, [P, I32, ctypes.c_uint64, P, P]),
+        "dgm_faces": (I32, [P, ctypes.POINTER(I64), P]),
+        "dgm_step_sc": (I32, [P, P, P, P, D, I64, I32, P]),
+        "dgm_rhs_sc": (I32, [P, P, P, P, P, P, P, P]),
+        "dgm_energy_sc": (I32, [P, P, P, P, P, P]),
         "dgm_tables": (I32, [P, P, P, P, P]),
         "dgm_match_faces_host": (I32, [ctypes.POINTER(_Mesh), P, P, P, P]),
         "dgm_last_launches": (I64, [P]),
@@ -103,7 +108,7 @@ def dgm_match_faces_host(xyz, tet, rep=None):
 class Context:
     """Owns a dgm_ctx.  Methods mirror the C ABI names (dgm_*)."""
 
-    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central"):
+    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0):
         lib = load_library()
         self._lib = lib
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
@@ -114,7 +119,7 @@ class Context:
         self._keep = (xyz, tet, repa, eps_a, mu_a)
         m = _Mesh(xyz.shape[0], xyz.ctypes.data, tet.shape[0], tet.ctypes.data,
                   None if repa is None else repa.ctypes.data)
-        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1))
+        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0))
         h = ctypes.c_void_p()
         st = lib.dgm_create(ctypes.byref(m), int(p), eps_a.ctypes.data, mu_a.ctypes.data, ctypes.byref(o), ctypes.byref(h))
         if st != DGM_OK:
@@ -183,6 +188,35 @@ class Context:
         out = ctypes.c_double()
         self._check(self._lib.dgm_energy(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
                                          ctypes.byref(out), _stream(stream)))
+        return out.value
+
+    # -- stabilised central flux (flux="stabilized") ---------------------------
+    def dgm_faces(self):
+        """(n_faces, face_id[n_tet,4]) of the stabilised flux's face unknowns."""
+        nf = ctypes.c_int64()
+        fid = np.empty((self.n_tet, 4), np.int32)
+        self._check(self._lib.dgm_faces(self.h, ctypes.byref(nf), fid.ctypes.data))
+        return nf.value, fid
+
+    def empty_faces(self):
+        import torch
+        nf, _ = self.dgm_faces()
+        NF = (self.p + 1) * (self.p + 2) // 2
+        return torch.zeros((nf, 2, NF), dtype=torch.float64, device="cuda")
+
+    def dgm_step_sc(self, E, H, HF, dt, nsteps=1, flags=0, stream=None):
+        self._check(self._lib.dgm_step_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
+                                          float(dt), int(nsteps), int(flags), _stream(stream)))
+
+    def dgm_rhs_sc(self, E, H, HF, dE=None, dH=None, dHF=None, stream=None):
+        self._check(self._lib.dgm_rhs_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
+                                         _ptr(self._field(dE, "dE")), _ptr(self._field(dH, "dH")), _ptr(dHF),
+                                         _stream(stream)))
+
+    def dgm_energy_sc(self, E, H, HF, stream=None):
+        out = ctypes.c_double()
+        self._check(self._lib.dgm_energy_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
+                                            ctypes.byref(out), _stream(stream)))
         return out.value
 
     def dgm_spectral_radius(self, iters=100, seed=0, stream=None):

@@ -92,6 +92,11 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_E);
   cudaFree(c->d_H);
   for (int i = 0; i < 3; ++i) cudaFree(c->d_pw[i]);
+  cudaFree(c->d_fid);
+  cudaFree(c->d_fside);
+  cudaFree(c->d_sign);
+  cudaFree(c->d_fgeo);
+  cudaFree(c->d_fnorms);
   if (c->side) cudaStreamDestroy(c->side);
   for (int i = 0; i < 4; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
@@ -105,8 +110,9 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   if (order < 1 || order > DGM_PMAX)
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
-  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0};
-  if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND) return dgm::set_err(c, DGM_EINVAL, "unknown flux");
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0};
+  if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
+    return dgm::set_err(c, DGM_EINVAL, "unknown flux");
   const int p = order;
   const int64_t n = m->n_tet;
   c->p = p;
@@ -243,6 +249,54 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   for (int64_t t = 0; t < n; ++t)
     for (int f = 0; f < 4; ++f) c->sign[4 * t + f] = (int8_t)((f % 2 == 0 ? 1 : -1) * sgn[t]);
 
+  // ---- stabilised central flux: face numbering and face geometry
+  if (o.flux == DGM_FLUX_STABILIZED) {
+    c->alpha = (o.alpha0 > 0 ? o.alpha0 : 1.0) * p * p;
+    c->fid.assign(n * 4, -1);
+    c->fside.clear();
+    for (int64_t t = 0; t < n; ++t)
+      for (int f = 0; f < 4; ++f) {
+        const int32_t nb = c->nbr[4 * t + f];
+        if (nb < 0 || t < nb) {
+          c->fid[4 * t + f] = (int32_t)(c->fside.size() / 2);
+          c->fside.push_back((int32_t)(4 * t + f));
+          c->fside.push_back(nb < 0 ? -1 : 4 * nb + c->nbrf[4 * t + f]);
+        }
+      }
+    for (int64_t t = 0; t < n; ++t)
+      for (int f = 0; f < 4; ++f)
+        if (c->fid[4 * t + f] < 0) c->fid[4 * t + f] = c->fid[4 * c->nbr[4 * t + f] + c->nbrf[4 * t + f]];
+    c->n_faces = (int64_t)c->fside.size() / 2;
+    c->fgeo.assign(c->n_faces * 8, 0.0);
+    for (int64_t k = 0; k < c->n_faces; ++k) {
+      const int64_t t = c->fside[2 * k] / 4;
+      const int f = c->fside[2 * k] % 4;
+      const int *fv = kFaceVerts[f];
+      double X[3][3];
+      for (int q = 0; q < 3; ++q)
+        for (int i = 0; i < 3; ++i) X[q][i] = m->xyz[3 * (int64_t)m->tet[4 * t + fv[q]] + i];
+      double t1[3], t2[3];
+      for (int i = 0; i < 3; ++i) {
+        t1[i] = X[1][i] - X[0][i];
+        t2[i] = X[2][i] - X[0][i];
+      }
+      const double g11 = t1[0] * t1[0] + t1[1] * t1[1] + t1[2] * t1[2];
+      const double g12 = t1[0] * t2[0] + t1[1] * t2[1] + t1[2] * t2[2];
+      const double g22 = t2[0] * t2[0] + t2[1] * t2[1] + t2[2] * t2[2];
+      const double cx = t1[1] * t2[2] - t1[2] * t2[1], cy = t1[2] * t2[0] - t1[0] * t2[2],
+                   cz = t1[0] * t2[1] - t1[1] * t2[0];
+      const double area = std::sqrt(cx * cx + cy * cy + cz * cz);
+      double *G = &c->fgeo[8 * k];
+      G[0] = g11 / area;   // M^{-1} = g / |t1×t2|
+      G[1] = g12 / area;
+      G[2] = g22 / area;
+      G[3] = std::sqrt(area) / c->alpha;   // h_F / α, h_F = sqrt(|t1×t2|) (reading G16)
+      G[4] = g22 / area;   // M = |t1×t2| g^{-1}
+      G[5] = -g12 / area;
+      G[6] = g11 / area;
+    }
+  }
+
   c->h_geo.swap(geo);
   c->h_fmet.swap(fmet);
   return DGM_OK;
@@ -263,6 +317,21 @@ dgm_status upload_impl(dgm_ctx *c) {
   if (c->flux == DGM_FLUX_UPWIND) {
     CUDA_TRY(c, cudaMalloc(&c->d_fmet, sizeof(double) * 12 * n));
     CUDA_TRY(c, cudaMemcpy(c->d_fmet, c->h_fmet.data(), sizeof(double) * 12 * n, cudaMemcpyHostToDevice));
+  }
+  if (c->flux == DGM_FLUX_STABILIZED) {
+    CUDA_TRY(c, cudaMalloc(&c->d_fid, 4 * sizeof(int32_t) * n));
+    CUDA_TRY(c, cudaMemcpy(c->d_fid, c->fid.data(), 4 * sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMalloc(&c->d_fside, 2 * sizeof(int32_t) * c->n_faces));
+    CUDA_TRY(c, cudaMemcpy(c->d_fside, c->fside.data(), 2 * sizeof(int32_t) * c->n_faces, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMalloc(&c->d_sign, 4 * n));
+    CUDA_TRY(c, cudaMemcpy(c->d_sign, c->sign.data(), 4 * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMalloc(&c->d_fgeo, 8 * sizeof(double) * c->n_faces));
+    CUDA_TRY(c, cudaMemcpy(c->d_fgeo, c->fgeo.data(), 8 * sizeof(double) * c->n_faces, cudaMemcpyHostToDevice));
+    std::vector<double> fn(c->NF);
+    for (int d = 0, q = 0; d <= p; ++d)
+      for (int mm = 0; mm <= d; ++mm, ++q) fn[q] = 1.0 / ((2.0 * mm + 1) * (2.0 * d + 2));   // ‖ψ_mn‖², n = d-m
+    CUDA_TRY(c, cudaMalloc(&c->d_fnorms, sizeof(double) * c->NF));
+    CUDA_TRY(c, cudaMemcpy(c->d_fnorms, fn.data(), sizeof(double) * c->NF, cudaMemcpyHostToDevice));
   }
   // trace buffers TE0, TE1, TH0, TH1 (the second of each only for upwind); the lane
   // path interleaves groups of 16 elements, so round up, plus 16 spare elements that
@@ -383,7 +452,9 @@ namespace {
 // stream right after the last H stage (H is final from then on).  If
 // before_entry is given the stream waits on it after the entry traces of E.
 dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps, int flags, cudaStream_t st,
-                     cudaEvent_t before_h, cudaEvent_t h_done) {
+                     cudaEvent_t before_h, cudaEvent_t h_done, double *HF = nullptr) {
+  if (c->flux == DGM_FLUX_STABILIZED && !HF)
+    return dgm::set_err(c, DGM_EINVAL, "stabilised contexts step through dgm_step_sc (the face unknowns H^F)");
   const bool up = c->flux == DGM_FLUX_UPWIND;
   int ce = 0, ch = 0;
   dgm_status r = DGM_OK;
@@ -402,9 +473,13 @@ dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps
     r = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
     if (up) ch = 1 - ch;
     if (r != DGM_OK) break;
+    // stabilised flux: H^F += dt Ḣ^F(E^n) from E's traces (before the E stage overwrites them)
+    if (HF && (r = dgm::launch_hf(c, TE, HF, nullptr, dt, st)) != DGM_OK) break;
     if (h_done && s == nsteps - 1) cudaEventRecord(h_done, st);
     double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
+    c->cur_HF = HF;
     r = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
+    c->cur_HF = nullptr;
     if (up) ce = 1 - ce;
   }
   if (r == DGM_OK) {
@@ -463,6 +538,53 @@ dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t 
   CUDA_TRY(c, cudaStreamSynchronize(st));
   c->tr_valid = false;   // the caller owns the host copies now
   return DGM_OK;
+}
+
+dgm_status dgm_faces(const dgm_ctx *c, int64_t *n_faces, int32_t *face_id) {
+  if (!c) return DGM_EINVAL;
+  if (c->flux != DGM_FLUX_STABILIZED) return DGM_EINVAL;
+  if (n_faces) *n_faces = c->n_faces;
+  if (face_id) std::memcpy(face_id, c->fid.data(), sizeof(int32_t) * 4 * c->n_tet);
+  return DGM_OK;
+}
+
+dgm_status dgm_step_sc(dgm_ctx *c, double *E, double *H, double *HF, double dt, int64_t nsteps, int flags,
+                       void *stream) {
+  if (!c || !E || !H || !HF || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
+  if (c->flux != DGM_FLUX_STABILIZED) return dgm::set_err(c, DGM_EINVAL, "context was not created with DGM_FLUX_STABILIZED");
+  c->launches = 0;
+  if (nsteps == 0) return DGM_OK;
+  return run_steps(c, E, H, dt, nsteps, flags, (cudaStream_t)stream, nullptr, nullptr, HF);
+}
+
+dgm_status dgm_rhs_sc(dgm_ctx *c, const double *E, const double *H, const double *HF, double *dE, double *dH,
+                      double *dHF, void *stream) {
+  if (!c || !E || !H || !HF) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  if (c->flux != DGM_FLUX_STABILIZED) return dgm::set_err(c, DGM_EINVAL, "context was not created with DGM_FLUX_STABILIZED");
+  cudaStream_t st = (cudaStream_t)stream;
+  c->launches = 0;
+  c->tr_valid = false;
+  double *TE = c->d_tr[0], *TH = c->d_tr[2];
+  dgm_status s = dgm::launch_tb_traces(c, E, TE, st);
+  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st);
+  if (s == DGM_OK && dH) s = dgm::launch_tb_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 1, dgm::OUT_WRITE, TE, TH, nullptr, st);
+  if (s == DGM_OK && dHF) s = dgm::launch_hf(c, TE, nullptr, dHF, 0.0, st);
+  if (s == DGM_OK && dE) {
+    c->cur_HF = HF;
+    s = dgm::launch_tb_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 1, 1, dgm::OUT_WRITE, TH, TE, nullptr, st);
+    c->cur_HF = nullptr;
+  }
+  return s;
+}
+
+dgm_status dgm_energy_sc(dgm_ctx *c, const double *E, const double *H, const double *HF, double *out, void *stream) {
+  if (!c || !E || !H || !HF || !out) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  if (c->flux != DGM_FLUX_STABILIZED) return dgm::set_err(c, DGM_EINVAL, "context was not created with DGM_FLUX_STABILIZED");
+  double w = 0.0, wf = 0.0;
+  dgm_status s = dgm::launch_energy(c, E, H, &w, (cudaStream_t)stream);
+  if (s == DGM_OK) s = dgm::launch_face_energy(c, HF, &wf, (cudaStream_t)stream);
+  if (s == DGM_OK) *out = w + wf;
+  return s;
 }
 
 dgm_status dgm_spectral_radius(dgm_ctx *c, int iters, uint64_t seed, double *rho_out, void *stream) {

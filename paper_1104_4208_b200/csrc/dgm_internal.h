@@ -81,6 +81,8 @@ struct StageArgs {
   const int32_t *nbr;    // [n][4], -1 PEC
   const int8_t *nbrf;    // [n][4], -1 PEC
   const double *fmet;    // upwind: [n][4][3] M00 M01 M11
+  const double *HF;      // stabilised flux, E stage: face unknowns [n_faces][2][NF] (else null)
+  const int32_t *fid;    // [n][4] face index
   int64_t n_tet;
   double dt;
   int stage, upwind, do_curl, do_flux, out_mode;
@@ -111,6 +113,16 @@ struct dgm_ctx {
   cudaStream_t side = nullptr;             // dgm_step_host: H copies overlap the kernels
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t launches = 0;
+  // stabilised central flux
+  int64_t n_faces = 0;
+  double alpha = 1.0;
+  std::vector<int32_t> fid;            // [n][4]
+  std::vector<int32_t> fside;          // [n_faces][2]: 4*tet+face of the two sides (-1: PEC)
+  std::vector<double> fgeo;            // [n_faces][8]: Minv00 Minv01 Minv11, h/α, M00 M01 M11, 0
+  int32_t *d_fid = nullptr, *d_fside = nullptr;
+  int8_t *d_sign = nullptr;
+  double *d_fgeo = nullptr, *d_fnorms = nullptr;
+  const double *cur_HF = nullptr;      // HF of the running *_sc call
   // trace-buffer state left by the last dgm_step (for DGM_STEP_CONTINUE)
   bool tr_valid = false;
   const double *tr_E = nullptr, *tr_H = nullptr;
@@ -127,6 +139,8 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
                            cudaStream_t st);
 dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
+dgm_status launch_hf(dgm_ctx *c, const double *TE, double *HF, double *dHF, double dt, cudaStream_t st);
+dgm_status launch_face_energy(dgm_ctx *c, const double *HF, double *out, cudaStream_t st);
 dgm_status launch_massdot(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out, cudaStream_t st);
 dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaStream_t st);
 dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);

@@ -288,7 +288,13 @@ __global__ void __launch_bounds__(Dim2<P>::W * 32)
           const double o1 = __ldg(to + gm), o2 = __ldg(to + NF + gm);
           const double n1 = nb >= 0 ? __ldg(tn + gm) : mirrorY * o1;
           const double n2 = nb >= 0 ? __ldg(tn + NF + gm) : mirrorY * o2;
-          double A = -sf * w * (n2 - o2), B = sf * w * (n1 - o1);
+          double h1 = 0.0, h2 = 0.0;   // stabilised flux (E stage): Δ_k -= H^F_k
+          if (a.HF) {
+            const double *hf = a.HF + (int64_t)a.fid[4 * e + f] * 2 * NF;
+            h1 = __ldg(hf + gm);
+            h2 = __ldg(hf + NF + gm);
+          }
+          double A = -sf * (w * (n2 - o2) - h2), B = sf * (w * (n1 - o1) - h1);
           if (UP) {
             const double *xo = a.trX + (e * 4 + f) * 2 * NF;
             const double xo1 = __ldg(xo + gm), xo2 = __ldg(xo + NF + gm);
@@ -502,6 +508,8 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
   a.dt = dt;
   a.stage = stage;
   a.upwind = c->flux == DGM_FLUX_UPWIND && do_flux;
+  a.HF = (stage == STAGE_E && do_flux) ? c->cur_HF : nullptr;
+  a.fid = c->d_fid;
   a.do_curl = do_curl;
   a.do_flux = do_flux;
   a.out_mode = out_mode;
@@ -572,6 +580,102 @@ __global__ void seed_kernel(double *X, uint64_t seed, int64_t n_tet, int N, int 
     z ^= z >> 31;
     X[i] = ((double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0) / (1.0 + al);
   }
+}
+
+// Stabilised central flux, face equation (signs reading G16):
+//   Ḣ^F_γ = (h_F/α) M^{-1} Σ_{T∋F} σ_{T,f} (E_2, -E_1)_{T,f,γ}
+// from the tangential traces of E in the trace buffer (both layouts); one thread per
+// (face, mode).  HF += dt Ḣ^F (update) or dHF = Ḣ^F (write).
+__global__ void hf_kernel(const double *__restrict__ TE, double *HF, double *dHF, double dt,
+                          const int32_t *__restrict__ fside, const int8_t *__restrict__ sign,
+                          const double *__restrict__ fgeo, int64_t n_faces, int NF, int lane_layout) {
+  const int64_t total = n_faces * NF;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / NF;
+    const int g = (int)(i - k * NF);
+    double r1 = 0.0, r2 = 0.0;
+    for (int sd = 0; sd < 2; ++sd) {
+      const int32_t tf = fside[2 * k + sd];
+      if (tf < 0) continue;
+      const int64_t e = tf >> 2;
+      const int f = tf & 3;
+      int64_t i1, i2;
+      if (lane_layout) {
+        i1 = (((e >> 4) * 8 * NF + (f * 2 + 0) * NF + g) << 4) + (e & 15);
+        i2 = (((e >> 4) * 8 * NF + (f * 2 + 1) * NF + g) << 4) + (e & 15);
+      } else {
+        i1 = (e * 4 + f) * 2 * NF + g;
+        i2 = i1 + NF;
+      }
+      const double sg = (double)sign[tf];
+      r1 += sg * __ldg(TE + i2);
+      r2 -= sg * __ldg(TE + i1);
+    }
+    const double *G = fgeo + 8 * k;
+    const double d1 = G[3] * (G[0] * r1 + G[1] * r2);
+    const double d2 = G[3] * (G[1] * r1 + G[2] * r2);
+    double *o = HF ? HF : dHF;
+    const int64_t b = k * 2 * NF + g;
+    if (HF) {
+      o[b] += dt * d1;
+      o[b + NF] += dt * d2;
+    } else {
+      o[b] = d1;
+      o[b + NF] = d2;
+    }
+  }
+}
+
+// ½ Σ_F (α/h_F) Σ_γ ‖ψ_γ‖² H_γᵀ M H_γ  (face part of the stabilised energy)
+__global__ void face_energy_kernel(const double *__restrict__ HF, const double *__restrict__ fgeo,
+                                   const double *__restrict__ fnorms, int64_t n_faces, int NF, double *partial) {
+  double sum = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_faces; k += (int64_t)gridDim.x * blockDim.x) {
+    const double *G = fgeo + 8 * k;
+    double q = 0.0;
+    for (int g = 0; g < NF; ++g) {
+      const double h1 = HF[k * 2 * NF + g], h2 = HF[k * 2 * NF + NF + g];
+      q += fnorms[g] * (G[4] * h1 * h1 + 2.0 * G[5] * h1 * h2 + G[6] * h2 * h2);
+    }
+    sum += 0.5 / G[3] * q;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+dgm_status launch_hf(dgm_ctx *c, const double *TE, double *HF, double *dHF, double dt, cudaStream_t st) {
+  if (c->n_faces == 0) return DGM_OK;
+  const int64_t total = c->n_faces * c->NF;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 8 * (int64_t)c->sms) grid = 8 * (int64_t)c->sms;
+  hf_kernel<<<(unsigned)grid, 256, 0, st>>>(TE, HF, dHF, dt, c->d_fside, c->d_sign, c->d_fgeo, c->n_faces, c->NF,
+                                            c->p <= kLanePmax ? 1 : 0);
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("hf_kernel: ") + cudaGetErrorString(e));
+}
+
+dgm_status launch_face_energy(dgm_ctx *c, const double *HF, double *out, cudaStream_t st) {
+  const int threads = 256;
+  int64_t grid = (c->n_faces + threads - 1) / threads;
+  if (grid > 4 * (int64_t)c->sms) grid = 4 * (int64_t)c->sms;
+  if (grid < 1) grid = 1;
+  if (c->n_partial < grid + 1) {
+    cudaFree(c->d_partial);
+    if (cudaMalloc(&c->d_partial, sizeof(double) * (grid + 1)) != cudaSuccess) return set_err(c, DGM_ENOMEM, "partials");
+    c->n_partial = grid + 1;
+  }
+  face_energy_kernel<<<(unsigned)grid, threads, 0, st>>>(HF, c->d_fgeo, c->d_fnorms, c->n_faces, c->NF, c->d_partial);
+  sum_kernel<<<1, 256, 0, st>>>(c->d_partial, (int)grid, c->d_partial + grid);
+  cudaError_t e = cudaMemcpyAsync(out, c->d_partial + grid, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("face_energy: ") + cudaGetErrorString(e));
 }
 
 template <int P>

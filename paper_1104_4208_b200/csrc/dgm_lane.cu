@@ -290,11 +290,13 @@ __global__ void __launch_bounds__(L2<P>::WARPS * 32)
             xo = a.trX + tix<NF>(ge, f, 0, 0);
             xn = nb >= 0 ? a.trX + tix<NF>(nb, gf, 0, 0) : nullptr;
           }
+          // stabilised flux (E stage): the face unknown enters as Δ_k -= H^F_k
+          const double *hfp = a.HF ? a.HF + ((int64_t)a.fid[4 * ge + f] * 2 + h) * NF : nullptr;
 #pragma unroll
           for (int gm = 0; gm < NF; ++gm) {
             const double t = q[gm];
             const double tnv = nb >= 0 ? cur[gm] : mirrorY * t;
-            double v = fs * w * (tnv - t);
+            double v = fs * (w * (tnv - t) - (hfp ? __ldg(hfp + gm) : 0.0));
             if (UP) {
               const double xo1 = __ldg(xo + 16 * gm), xo2 = __ldg(xo + 16 * (NF + gm));
               const double xn1 = nb >= 0 ? __ldg(xn + 16 * gm) : mirrorX * xo1;
@@ -459,6 +461,8 @@ dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, 
   a.dt = dt;
   a.stage = stage;
   a.upwind = c->flux == DGM_FLUX_UPWIND && do_flux;
+  a.HF = (stage == STAGE_E && do_flux) ? c->cur_HF : nullptr;
+  a.fid = c->d_fid;
   a.do_curl = do_curl;
   a.do_flux = do_flux;
   a.out_mode = out_mode;

@@ -1,0 +1,109 @@
+"""GPU parity of the stabilised central flux with face unknowns H^F (NEXT-1;
+PAPER.md:199-239, readings G16-G17) against oracle.tier_b.TierBStab, through
+the C-ABI (dgm_faces, dgm_rhs_sc, dgm_step_sc, dgm_energy_sc)."""
+import numpy as np
+import pytest
+
+import dgm_inputs as di
+from oracle.tier_b import TierBStab, symplectic_euler_stab
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need CUDA (no CPU fallback exists)"
+
+
+def _rel(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def _case(p, periodic, n, seed=5, alpha0=1.0):
+    import torch
+    from paper_1104_4208_b200 import Context
+    m = di.kuhn_mesh(n, periodic=periodic, jitter=0.1, seed=seed)
+    rep = m.rep if any(periodic) else None
+    rng = np.random.default_rng(seed)
+    eps, mu = rng.uniform(1, 4, m.n_tet), rng.uniform(1, 2, m.n_tet)
+    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux="stabilized", alpha0=alpha0)
+    B = TierBStab(m.xyz, m.tet, rep, p, eps, mu, alpha0=alpha0)
+    E = rng.standard_normal((3, m.n_tet, c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N))
+    NF = (p + 1) * (p + 2) // 2
+    HF = rng.standard_normal((B.n_faces, 2, NF))
+    return m, c, B, E, H, HF
+
+
+def _dev(c, X):
+    import torch
+    D = c.empty_field()
+    D[:, :, :c.N] = torch.as_tensor(X, device="cuda")
+    return D
+
+
+CASES = [(p, (False,) * 3, 2) for p in (1, 2, 3, 4, 5, 6, 7, 8)] + \
+        [(3, (True,) * 3, 3), (6, (False, True, True), 3), (7, (True, False, True), 3)]
+
+
+@pytest.mark.parametrize("p,periodic,n", CASES)
+def test_stab_faces_and_rhs_parity(p, periodic, n):
+    import torch
+    m, c, B, E, H, HF = _case(p, periodic, n)
+    nf, fid = c.dgm_faces()
+    assert nf == B.n_faces
+    assert np.array_equal(fid, B.fid)
+    Ed, Hd = _dev(c, E), _dev(c, H)
+    HFd = torch.as_tensor(HF, device="cuda").contiguous()
+    dE, dH = c.empty_field(), c.empty_field()
+    dHF = torch.empty_like(HFd)
+    c.dgm_rhs_sc(Ed, Hd, HFd, dE, dH, dHF)
+    assert _rel(dE[:, :, :c.N].cpu().numpy(), B.dE(E, H, HF)) <= 1e-12
+    assert _rel(dH[:, :, :c.N].cpu().numpy(), B.dH(E, H)) <= 1e-12
+    assert _rel(dHF.cpu().numpy(), B.dHF(E)) <= 1e-12
+    w = c.dgm_energy_sc(Ed, Hd, HFd)
+    assert w == pytest.approx(B.energy(E, H, HF), rel=1e-12)
+
+
+@pytest.mark.parametrize("p,periodic,n", [(2, (False,) * 3, 2), (4, (True,) * 3, 3), (7, (False,) * 3, 2)])
+def test_stab_steps_parity_and_energy(p, periodic, n):
+    """100 symplectic-Euler steps with (H, H^F) advanced together vs the oracle
+    (≤1e-10), then the discrete energy stays bounded (leapfrog on a skew system)."""
+    import torch
+    m, c, B, E, H, HF = _case(p, periodic, n, seed=7, alpha0=2.0)
+    Ed, Hd = _dev(c, E), _dev(c, H)
+    HFd = torch.as_tensor(HF, device="cuda").contiguous()
+    rho = c.dgm_spectral_radius(iters=60)
+    dt = 0.2 / np.sqrt(rho)
+    w0 = c.dgm_energy_sc(Ed, Hd, HFd)
+    c.dgm_step_sc(Ed, Hd, HFd, dt, 100)
+    E1, H1, HF1 = symplectic_euler_stab(B, E, H, HF, dt, 100)
+    assert _rel(Ed[:, :, :c.N].cpu().numpy(), E1) <= 1e-10
+    assert _rel(Hd[:, :, :c.N].cpu().numpy(), H1) <= 1e-10
+    assert _rel(HFd.cpu().numpy(), HF1) <= 1e-10
+    w1 = c.dgm_energy_sc(Ed, Hd, HFd)
+    assert w1 == pytest.approx(B.energy(E1, H1, HF1), rel=1e-11)
+    assert abs(w1 - w0) <= 0.05 * w0
+
+
+def test_stab_continue_mode_matches_fresh():
+    import torch
+    from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
+    m, c, B, E, H, HF = _case(5, (True,) * 3, 3, seed=9)
+    Ed, Hd = _dev(c, E), _dev(c, H)
+    HFd = torch.as_tensor(HF, device="cuda").contiguous()
+    dt = 1e-3
+    c.dgm_step_sc(Ed, Hd, HFd, dt, 3)
+    c.dgm_step_sc(Ed, Hd, HFd, dt, 4, DGM_STEP_CONTINUE)
+    E1, H1, HF1 = symplectic_euler_stab(B, E, H, HF, dt, 7)
+    assert _rel(Ed[:, :, :c.N].cpu().numpy(), E1) <= 1e-11
+    assert _rel(HFd.cpu().numpy(), HF1) <= 1e-11
+
+
+def test_stab_context_rejects_plain_step():
+    from paper_1104_4208_b200.binding import DgmError
+    m, c, B, E, H, HF = _case(2, (False,) * 3, 2)
+    Ed, Hd = _dev(c, E), _dev(c, H)
+    with pytest.raises(DgmError):
+        c.dgm_step(Ed, Hd, 1e-3, 1)
