@@ -195,26 +195,32 @@ def run_ours(args, rank, world):
     res = dict(value=value, ms_per_step=ms_per_step, launches=launches, clocks=clk.summary(), N=N, n_tet=n,
                l2=("flushed (512 MiB write) between steps" if flush_needed else
                    f"state {state_bytes / 1e9:.2f} GB > 2x L2: no flush"))
-    # roofline of the dominant kernel: with DGM_STEP_CONTINUE a step is exactly two
-    # stage-kernel launches (H stage, E stage)
+    # roofline of the operator application per stage.  With DGM_STEP_CONTINUE a step
+    # is two stages: sparse = one stage kernel each; dense = flux + stage GEMM + trace
+    # GEMM each (the "launch" below is then the whole stage, timed as step/2)
     upwind = cfg["flux"] == "upwind"
     per_launch_s = (t_total / args.steps) / 2
     B = algorithmic_bytes_per_stage(n, N, upwind)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    kern = "lane_stage_kernel" if p <= 6 else "stage2_kernel"
+    engine = ctx.engine
+    if engine == "dense":
+        kern = f"dense stage<{p}> (dense_flux_kernel + gemm_kernel<stage> + gemm_kernel<trace>)"
+    else:
+        kern = f"{'lane_stage_kernel' if p <= 6 else 'stream_kernel'}<{p}>"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f).get(args.config)
-        if tr and tr.get("kernel") == f"{'lane_stage_kernel' if p <= 6 else 'stage2_kernel'}<{p}>":
+        if tr and tr.get("kernel") == kern:
             traffic = tr["dram_bytes_per_launch"]
+    res["engine"] = engine
     res["roofline"] = {"bound": "hbm", "achieved": B / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
                        "frac": (B / per_launch_s / 1e9) / hbm, "traffic": traffic,
                        "traffic_source": "profiles/r01_traffic.json (one ncu --set full capture, bytes per launch)"
                        if traffic is not None else None,
-                       "kernel": f"{kern}<{p}>", "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
+                       "kernel": kern, "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
                        "launches_per_step": launches / args.steps,
                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
     # e2e through the C ABI with HOST buffers: H2D of E,H, the step, D2H of E,H
@@ -323,6 +329,7 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": args.config, "n_tet": res["n_tet"], "p": cfg["p"], "N": res["N"],
                            "flux": cfg["flux"], "periodic": cfg["periodic"], "l2": res["l2"],
+                           "engine": res["engine"],
                            "parallelism": "replicas only" if world > 1 else "single GPU",
                            "fields": "seeded random coefficients (C3 recipe); timing is data independent"},
                 "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["launches"]}

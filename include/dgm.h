@@ -77,11 +77,25 @@ typedef struct {
   const int32_t *rep;   /* [n_vert] host, periodic representative; NULL = id  */
 } dgm_mesh;
 
+/* Execution engine of the stage kernels.  Both compute the same operator (same
+ * flux, traces, lift, update; parity-tested against the oracle); they differ in how
+ * the reference-frame operators are applied:
+ *   SPARSE: the paper's recurrence sweeps and sum-factorised traces/lifts
+ *            as generated straight-line code (p <= 6) or a
+ *           streamed-table interpreter (p >= 7);
+ *   DENSE:  the same operators assembled once per context into matrices (from the
+ *           exact programs) and applied as block-sparse FP64 tensor-core GEMMs over
+ *           tiles of elements (mma.sync m8n8k4), 3 launches per stage.
+ *   AUTO:   SPARSE for p <= 5, DENSE for p >= 6 (measured faster there).
+ * The environment variable DGM_ENGINE=sparse|dense overrides AUTO. */
+typedef enum { DGM_ENGINE_AUTO = 0, DGM_ENGINE_SPARSE = 1, DGM_ENGINE_DENSE = 2 } dgm_engine_kind;
+
 typedef struct {
   int32_t flux;          /* dgm_flux                                          */
   int32_t eps_per_elem;  /* 0: eps points to one double; 1: to [n_tet]        */
   int32_t mu_per_elem;   /* same for mu                                       */
   double alpha0;         /* DGM_FLUX_STABILIZED: α = alpha0·p² (≤0 → 1)       */
+  int32_t engine;        /* dgm_engine_kind                                   */
 } dgm_opts;
 
 /* Validate the mesh, match faces, compute per-element geometry
@@ -191,6 +205,9 @@ dgm_status dgm_match_faces_host(const dgm_mesh *mesh, int32_t *nbr, int8_t *nbr_
 
 /* Number of kernel launches the last dgm_step/dgm_apply_* call enqueued. */
 int64_t dgm_last_launches(const dgm_ctx *ctx);
+
+/* The engine the context resolved to (DGM_ENGINE_SPARSE or DGM_ENGINE_DENSE). */
+int dgm_engine(const dgm_ctx *ctx);
 
 const char *dgm_last_error(const dgm_ctx *ctx);
 void dgm_destroy(dgm_ctx *ctx);

@@ -18,9 +18,10 @@ LIB_PATH = os.path.join(HERE, "libdgm.so")
 DGM_OK, DGM_EINVAL, DGM_EMESH, DGM_EORDER, DGM_ECUDA, DGM_ENOMEM = range(6)
 STATUS = {0: "DGM_OK", 1: "DGM_EINVAL", 2: "DGM_EMESH", 3: "DGM_EORDER", 4: "DGM_ECUDA", 5: "DGM_ENOMEM"}
 FLUX = {"central": 0, "upwind": 1, "stabilized": 2}
+ENGINE = {"auto": 0, "sparse": 1, "dense": 2}
 DGM_STEP_CONTINUE = 1
 EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
-           "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_last_error", "dgm_destroy"]
+           "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_engine", "dgm_last_error", "dgm_destroy"]
 
 
 class DgmError(RuntimeError):
@@ -36,7 +37,7 @@ class _Mesh(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32),
-                ("alpha0", ctypes.c_double)]
+                ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32)]
 
 
 _lib = None
@@ -68,6 +69,7 @@ def load_library(path: str = LIB_PATH):
         "dgm_tables": (I32, [P, P, P, P, P]),
         "dgm_match_faces_host": (I32, [ctypes.POINTER(_Mesh), P, P, P, P]),
         "dgm_last_launches": (I64, [P]),
+        "dgm_engine": (I32, [P]),
         "dgm_last_error": (ctypes.c_char_p, [P]),
         "dgm_destroy": (None, [P]),
     }
@@ -108,7 +110,7 @@ def dgm_match_faces_host(xyz, tet, rep=None):
 class Context:
     """Owns a dgm_ctx.  Methods mirror the C ABI names (dgm_*)."""
 
-    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0):
+    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0, engine="auto"):
         lib = load_library()
         self._lib = lib
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
@@ -119,7 +121,7 @@ class Context:
         self._keep = (xyz, tet, repa, eps_a, mu_a)
         m = _Mesh(xyz.shape[0], xyz.ctypes.data, tet.shape[0], tet.ctypes.data,
                   None if repa is None else repa.ctypes.data)
-        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0))
+        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0), ENGINE[engine])
         h = ctypes.c_void_p()
         st = lib.dgm_create(ctypes.byref(m), int(p), eps_a.ctypes.data, mu_a.ctypes.data, ctypes.byref(o), ctypes.byref(h))
         if st != DGM_OK:
@@ -241,6 +243,11 @@ class Context:
         bc = np.empty((n, 4), np.int8)
         self._check(self._lib.dgm_tables(self.h, nbr.ctypes.data, nf.ctypes.data, sg.ctypes.data, bc.ctypes.data))
         return nbr, nf, sg, bc
+
+    @property
+    def engine(self):
+        """'sparse' or 'dense': the engine this context resolved to (dgm_engine)."""
+        return {1: "sparse", 2: "dense"}[self._lib.dgm_engine(self.h)]
 
     def dgm_last_launches(self):
         return int(self._lib.dgm_last_launches(self.h))

@@ -41,14 +41,14 @@ def build(force=False, verbose=False):
     from .gen import lanegen
     if force or _stale(os.path.join(lanedir, f"lane_p{LANE_PMAX}.cuh"), [os.path.join(HERE, "gen", "lanegen.py"), inc]):
         lanegen.emit_all(lanedir, LANE_PMAX)
-    srcs = [os.path.join(CSRC, f) for f in ("dgm_host.cpp", "dgm_kernels.cu", "dgm_lane.cu")]
+    srcs = [os.path.join(CSRC, f) for f in ("dgm_host.cpp", "dgm_kernels.cu", "dgm_lane.cu", "dgm_stream.cu", "dgm_dense.cu")]
     deps = srcs + [inc, os.path.join(CSRC, "dgm_internal.h"), os.path.join(HERE, "..", "include", "dgm.h"),
                    os.path.join(lanedir, f"lane_p{LANE_PMAX}.cuh")]
     if not force and not _stale(LIB, deps):
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-x", "cu", srcs[0], "-x", "cu", srcs[1], "-x", "cu", srcs[2],
+           "-Xptxas", "-v" if verbose else "-O3", *[a for f in srcs for a in ("-x", "cu", f)],
            "-o", LIB, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -1,0 +1,432 @@
+// Dense-contraction stage engine (FP64 tensor cores, mma.sync m8n8k4), sm_100a.
+//
+// The per-element operator is linear in the reference frame:
+//   acc_T = Ĉ Ŷ_T + Σ_f L_f (A_f, B_f)_T,   Ẋ_T = ±(1/m_T) G'_T acc_T,
+//   traces_T = Tr X_T,
+// with Ĉ the reference curl, L_f the lift and Tr the tangential
+// face traces.  Ĉ, L, Tr are the SAME matrices for every element,
+// so applied to a tile of elements they are GEMMs: M = elements, N = output modes,
+// K = input modes.  The matrices are assembled once per context from the exact
+// recurrence / staged-trace programs (dgm_host.cpp: dense_build), so this engine
+// computes the same operator as the sparse kernels with a different summation order.
+//
+// Why: the sparse recurrence path needs ~10x fewer flops, but every FMA of it reads
+// its operand from shared memory (no register reuse), which caps it near 5-10 % of
+// the FP64 pipe at p >= 7 (profiles/).  A register-blocked DMMA GEMM re-uses each
+// operand from registers 6-8 times.  NORTH_STAR allows tensor cores where a dense
+// contraction is measured to beat the sparse path; bench.py reports which engine ran.
+//
+// Per stage (E or H), three launches:
+//   dense_flux_kernel   A, B face fields from the trace buffers (central/upwind/
+//                       stabilised, PEC mirror), AB[e][(f*2+{A,B})*NF + γ]
+//   gemm<EPI_STAGE>     acc = [Ŷ | AB] · B1, epilogue G'-mix, ±1/m, X += dt Ẋ (or write)
+//   gemm<EPI_TRACE>     traces of the updated X = X · B2 -> trace buffer tr[e][f][k][γ]
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+
+#include "dgm_internal.h"
+
+namespace dgm {
+namespace {
+
+constexpr int BN = 96, BK = 16;
+constexpr int WM = 32, WN = 32;   // warp tile: 4 x 4 MMAs of 8x8; the 3 warp columns = the 3 column blocks
+constexpr int BST = BN + 4;       // padded smem strides (conflict-free fragment loads)
+
+// CTA shape: BM elements x BN columns, (BM/32) x 2 warps, NST-stage cp.async pipeline
+template <int BM_, int NST_>
+struct Cfg {
+  static constexpr int BM = BM_, NSTAGE = NST_, AST = BM_ + 4, NTHREADS = (BM_ / WM) * (BN / WN) * 32;
+  static constexpr int MINB = BM_ == 64 ? (NST_ <= 3 ? 3 : 2) : 1;
+  struct Smem {
+    double A[NST_][BK][AST];
+    double B[NST_][BK][BST];
+  };
+  static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * BST + BM_ * 8);   // C tile + geometry rows
+  static constexpr size_t SMEM = sizeof(Smem) > EPI_BYTES ? sizeof(Smem) : EPI_BYTES;
+};
+
+enum { EPI_STAGE = 0, EPI_TRACE = 1 };
+
+struct GemmArgs {
+  // A operand, element e, column k (component-blocked rows, see DenseOps):
+  //   k <  k1: c = k / Nk, β = k % Nk  -> p0 + e*ld0 + c*cs + β      (β < N, else 0)
+  //   k >= k1: j = (k-k1) / NFk, γ = ..  -> p1 + e*ld1 + j*NF + γ     (γ < NF, j < 8, else 0)
+  const double *p0, *p1;
+  int64_t ld0, ld1, cs;
+  int k1, Nk, NFk;
+  // B operand: [Kpad][NC] row-major; per n-tile the list of non-zero k-tiles
+  const double *Bm;
+  int NC;
+  int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t gathers β in [32t, 32t+32)
+  const uint32_t *ktl;     // per non-zero k-tile: kt | (12-bit mask of non-zero 16x8 column groups) << 16
+  const int32_t *ktoff;
+  int ntiles_n;
+  int64_t n_tet;
+  // epilogue
+  int N, NF, LD;
+  int ncols;   // valid output columns (EPI_TRACE: 8NF)
+  const Geo *geo;
+  double *X, *dX, *tr;
+  const double *Xin;   // (unused by the GEMM; kept for symmetry)
+  double dt;
+  int stageE, out_mode;
+};
+
+__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cpa8(double *dst, const double *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cpa16(double *dst, const double *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NW>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NW) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// load k-tile kt of the A (transposed to [k][m]) and B operands into stage buffer st
+template <int EPI, class C>
+__device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, int st, int64_t m0, int nt, int kt,
+                                          int tid) {
+  constexpr int BM = C::BM, NTHREADS = C::NTHREADS;
+  const int kk = tid & (BK - 1);
+  const int k = kt * BK + kk;
+  int64_t ko = -1;
+  const bool lo = k < g.k1;
+  if (lo) {
+    const int c = k / g.Nk, b = k - c * g.Nk;
+    if (b < g.N) ko = c * g.cs + b;
+  } else {
+    const int j = (k - g.k1) / g.NFk, gm = (k - g.k1) - j * g.NFk;
+    if (gm < g.NF && j < 8) ko = (int64_t)j * g.NF + gm;
+  }
+  const double *base = lo ? g.p0 : g.p1;
+  const int64_t ld = lo ? g.ld0 : g.ld1;
+  for (int m = tid >> 4; m < BM; m += NTHREADS / BK) {
+    const int64_t e = m0 + m;
+    const bool ok = ko >= 0 && e < g.n_tet;
+    cpa8(&sm.A[st][kk][m], ok ? base + e * ld + ko : g.p0, ok);
+  }
+  const double *bsrc = g.Bm + (int64_t)kt * BK * g.NC;
+#pragma unroll
+  for (int i = 0; i < BK * BN / 2 / NTHREADS; ++i) {
+    const int idx = tid + i * NTHREADS;
+    const int r = idx / (BN / 2), c2 = idx - r * (BN / 2);
+    // EPI_STAGE gathers the three component blocks of modes [32nt, 32nt+32); traces are contiguous
+    const int col = EPI == EPI_STAGE ? (c2 >> 4) * g.Np + 32 * nt + 2 * (c2 & 15) : nt * BN + 2 * c2;
+    cpa16(&sm.B[st][r][2 * c2], bsrc + (int64_t)r * g.NC + col);
+  }
+}
+
+template <int EPI, class C>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) {
+  constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS, WMN = BM / WM;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  typename C::Smem &sm = *reinterpret_cast<typename C::Smem *>(dsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WMN, wn = warp / WMN;
+  const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
+  const int64_t mtiles = (g.n_tet + BM - 1) / BM;
+  const int64_t ntile_total = mtiles * g.ntiles_n;
+  for (int64_t t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+    const int64_t m0 = (t / g.ntiles_n) * BM;
+    const int nt = (int)(t % g.ntiles_n);
+    const int n0 = nt * BN;
+    const uint32_t *kts = g.ktl + g.ktoff[nt];
+    const int nk = g.ktoff[nt + 1] - g.ktoff[nt];
+    double acc[4][4][2];   // [column group j][row group i][pair]
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
+    // prologue
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) {
+      if (s < nk) load_tile<EPI, C>(g, sm, s, m0, nt, (int)(kts[s] & 0xFFFFu), tid);
+      cp_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+      cp_wait<NSTAGE - 2>();
+      __syncthreads();
+      const int nx = it + NSTAGE - 1;
+      if (nx < nk) load_tile<EPI, C>(g, sm, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFFFu), tid);
+      cp_commit();
+      const int st = it % NSTAGE;
+      // skip this warp's 16x32 operator block when it is zero (warp-uniform branch
+      // around the whole k-tile, so the tensor pipe is not occupied)
+      if ((kts[it] >> (16 + wn)) & 1u) {
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = sm.A[st][k4 * 4 + gc][wm * WM + i * 8 + gr];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = sm.B[st][k4 * 4 + gc][wn * WN + j * 8 + gr];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dmma(acc[j][i][0], acc[j][i][1], a[i], b[j]);
+        }
+      }
+    }
+    cp_wait<0>();
+    __syncthreads();
+    if (EPI == EPI_TRACE) {
+      // C fragment: row gr (+8i), cols 2gc, 2gc+1 (+8j) -> tr[e][col]
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t e = m0 + wm * WM + i * 8 + gr;
+        if (e >= g.n_tet) continue;
+        double *row = g.tr + e * (int64_t)g.ncols;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = n0 + wn * WN + j * 8 + 2 * gc;
+          if (col + 1 < g.ncols) {
+            *reinterpret_cast<double2 *>(row + col) = make_double2(acc[j][i][0], acc[j][i][1]);
+          } else if (col < g.ncols) {
+            row[col] = acc[j][i][0];
+          }
+        }
+      }
+    } else {
+      // stage the tile in shared memory, then per (element, mode): G' mix and update
+      double(*Cs)[BST] = reinterpret_cast<double(*)[BST]>(dsm);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = wm * WM + i * 8 + gr, c = wn * WN + j * 8 + 2 * gc;
+          Cs[r][c] = acc[j][i][0];
+          Cs[r][c + 1] = acc[j][i][1];
+        }
+      // per-element geometry rows after the tile: G' (6), ±1/m
+      double(*Gs)[8] = reinterpret_cast<double(*)[8]>(dsm + sizeof(double) * BM * BST);
+      for (int r = tid; r < BM; r += NTHREADS) {
+        const int64_t e = m0 + r;
+        if (e < g.n_tet) {
+          const Geo &G = g.geo[e];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) Gs[r][q] = G.g[q];
+          Gs[r][6] = g.stageE ? G.inv_eps : -G.inv_mu;
+        }
+      }
+      __syncthreads();
+      constexpr int MODES = BN / 3;
+      const int64_t cs = g.n_tet * g.LD;
+#pragma unroll 4
+      for (int idx = tid; idx < BM * MODES; idx += NTHREADS) {
+        const int r = idx / MODES, ml = idx - r * MODES;
+        const int64_t e = m0 + r;
+        const int b = 32 * nt + ml;
+        if (e >= g.n_tet || b >= g.N) continue;
+        const double *G = Gs[r];
+        const double cm = G[6];
+        const double v0 = Cs[r][ml], v1 = Cs[r][32 + ml], v2 = Cs[r][64 + ml];
+        const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
+        const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
+        const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
+        const int64_t o = e * g.LD + b;
+        if (g.out_mode == OUT_UPDATE) {
+          g.X[o] += g.dt * x0;
+          g.X[cs + o] += g.dt * x1;
+          g.X[2 * cs + o] += g.dt * x2;
+        } else if (g.out_mode == OUT_WRITE) {
+          g.dX[o] = x0;
+          g.dX[cs + o] = x1;
+          g.dX[2 * cs + o] = x2;
+        } else {
+          g.dX[o] += x0;
+          g.dX[cs + o] += x1;
+          g.dX[2 * cs + o] += x2;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// A, B face fields of every (element, face, mode) from the trace buffers
+// (tr[e][f][k][γ]); same flux as the stage kernels (reading G1/G2/G17).
+template <bool UP>
+__global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, double *__restrict__ AB, int NF) {
+  const int64_t total = a.n_tet * 4 * NF;
+  const bool stageE = a.stage == STAGE_E;
+  const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ef = i / NF;
+    const int gm = (int)(i - ef * NF);
+    const int64_t e = ef >> 2;
+    const int f = (int)(ef & 3);
+    const int nb = a.nbr[ef];
+    const int gf = a.nbrf[ef];
+    double w = 0.5, kk = 0.0;
+    if (UP) {
+      const double Zm = a.geo[e].Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
+      if (stageE) {
+        w = Zp / (Zm + Zp);
+        kk = 1.0 / (Zm + Zp);
+      } else {
+        const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
+        w = Yp / (Ym + Yp);
+        kk = 1.0 / (Ym + Yp);
+      }
+    }
+    const double sf = (f & 1) ? -1.0 : 1.0;
+    const double *to = trY + ef * 2 * NF;
+    const double o1 = __ldg(to + gm), o2 = __ldg(to + NF + gm);
+    double n1, n2;
+    if (nb >= 0) {
+      const double *tn = trY + ((int64_t)nb * 4 + gf) * 2 * NF;
+      n1 = __ldg(tn + gm);
+      n2 = __ldg(tn + NF + gm);
+    } else {
+      n1 = mirrorY * o1;
+      n2 = mirrorY * o2;
+    }
+    double h1 = 0.0, h2 = 0.0;   // stabilised flux (E stage): Δ_k -= H^F_k
+    if (a.HF) {
+      const double *hf = a.HF + (int64_t)a.fid[ef] * 2 * NF;
+      h1 = __ldg(hf + gm);
+      h2 = __ldg(hf + NF + gm);
+    }
+    double A = -sf * (w * (n2 - o2) - h2), B = sf * (w * (n1 - o1) - h1);
+    if (UP) {
+      const double *xo = a.trX + ef * 2 * NF;
+      const double xo1 = __ldg(xo + gm), xo2 = __ldg(xo + NF + gm);
+      double xn1, xn2;
+      if (nb >= 0) {
+        const double *xn = a.trX + ((int64_t)nb * 4 + gf) * 2 * NF;
+        xn1 = __ldg(xn + gm);
+        xn2 = __ldg(xn + NF + gm);
+      } else {
+        xn1 = mirrorX * xo1;
+        xn2 = mirrorX * xo2;
+      }
+      const double j1 = kk * (xn1 - xo1), j2 = kk * (xn2 - xo2);
+      const double *M = a.fmet + 12 * e + 3 * f;
+      const double ps = (stageE ? 1.0 : -1.0) * (a.geo[e].detF > 0 ? 1.0 : -1.0);
+      A += ps * (j1 * M[0] + j2 * M[1]);
+      B += ps * (j1 * M[1] + j2 * M[2]);
+    }
+    double *o = AB + ef * 2 * NF;
+    o[gm] = A;
+    o[NF + gm] = B;
+  }
+}
+
+template <int EPI, class C>
+dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
+  const size_t smem = C::SMEM;
+  auto kern = gemm_kernel<EPI, C>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NTHREADS, smem);
+  if (occ < 1) occ = 1;
+  const int64_t tiles = (g.n_tet + C::BM - 1) / C::BM * g.ntiles_n;
+  int64_t grid = (int64_t)c->sms * occ;
+  if (grid > tiles) grid = tiles;
+  kern<<<(unsigned)grid, C::NTHREADS, smem, st>>>(g);
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("gemm_kernel: ") + cudaGetErrorString(e));
+}
+
+int dense_cfg() {
+  const char *v = std::getenv("DGM_DENSE_CFG");
+  return v && *v ? std::atoi(v) : 0;
+}
+
+template <int EPI>
+dgm_status gemm_go(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
+  switch (dense_cfg()) {
+    case 1: return gemm_go_c<EPI, Cfg<64, 4>>(c, g, st);
+    case 2: return gemm_go_c<EPI, Cfg<128, 3>>(c, g, st);
+    case 3: return gemm_go_c<EPI, Cfg<128, 4>>(c, g, st);
+    default: return gemm_go_c<EPI, Cfg<64, 3>>(c, g, st);
+  }
+}
+
+}  // namespace
+
+dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
+  const DenseOps &D = c->dense;
+  if (a.do_flux) {
+    const int64_t total = a.n_tet * 4 * c->NF;
+    int64_t grid = (total + 255) / 256;
+    if (grid > 16 * (int64_t)c->sms) grid = 16 * (int64_t)c->sms;
+    if (a.upwind)
+      dense_flux_kernel<true><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF);
+    else
+      dense_flux_kernel<false><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF);
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("dense_flux_kernel: ") + cudaGetErrorString(e));
+  }
+  GemmArgs g{};
+  g.p0 = a.Y;
+  g.p1 = D.AB;
+  g.ld0 = c->LD;
+  g.ld1 = 8 * c->NF;
+  g.cs = c->n_tet * c->LD;
+  g.k1 = D.k1a;
+  g.Nk = D.k1a / 3;
+  g.NFk = (c->NF + BK - 1) / BK * BK;
+  g.Bm = D.B1;
+  g.NC = D.nc1;
+  g.Np = D.nc1 / 3;
+  // curl only / flux only: restrict the k-tile lists
+  const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
+  g.ktl = D.ktl1[sel];
+  g.ktoff = D.ktoff1[sel];
+  g.ntiles_n = D.nc1 / 3 / 32;
+  g.n_tet = c->n_tet;
+  g.N = c->N;
+  g.NF = c->NF;
+  g.LD = c->LD;
+  g.ncols = 3 * c->N;
+  g.geo = c->d_geo;
+  g.X = a.X;
+  g.dX = a.dX;
+  g.dt = a.dt;
+  g.stageE = a.stage == STAGE_E;
+  g.out_mode = a.out_mode;
+  dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
+  if (s != DGM_OK) return s;
+  if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st);
+  return DGM_OK;
+}
+
+dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
+  const DenseOps &D = c->dense;
+  GemmArgs g{};
+  g.p0 = X;
+  g.p1 = X;
+  g.ld0 = g.ld1 = c->LD;
+  g.cs = c->n_tet * c->LD;
+  g.k1 = 1 << 30;
+  g.Nk = D.k1a / 3;
+  g.NFk = (c->NF + BK - 1) / BK * BK;
+  g.Bm = D.B2;
+  g.NC = D.nc2;
+  g.ktl = D.ktl2;
+  g.ktoff = D.ktoff2;
+  g.ntiles_n = D.nc2 / BN;
+  g.n_tet = c->n_tet;
+  g.N = c->N;
+  g.NF = c->NF;
+  g.LD = c->LD;
+  g.ncols = 8 * c->NF;
+  g.tr = tr;
+  return gemm_go<EPI_TRACE>(c, g, st);
+}
+
+}  // namespace dgm

@@ -2,7 +2,9 @@
 // upload and the call wrappers (SURVEY.md §3 call stacks 1-4).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -49,7 +51,8 @@ const int kFaceVerts[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
 size_t prog_bytes(const HostProg &p) {
   size_t rows = (size_t)p.npass * 32, terms = (size_t)p.nterm * 32;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  return al(rows * 2) * 2 + al(terms * 2) + al(terms * 8) + al((p.npass + 1) * 4) + al(p.npass + 1) + al(terms * 16);
+  return al(rows * 2) * 2 + al(terms * 2) + al(terms * 8) + al((p.npass + 1) * 4) + al(p.npass + 1) + al(terms * 16) +
+         al(rows * 8) + al((p.npass + 1) * 8);
 }
 
 // Copy one program into the staging buffer at *off, return its device view.
@@ -77,11 +80,287 @@ dgm::DevProg stage_prog(const HostProg &p, std::vector<char> &buf, size_t &off, 
     std::memcpy(&packed[2 * q + 1], &sv, 8);
   }
   d.term = (const double2 *)put(packed.data(), terms * 16);
+  std::vector<uint32_t> meta(rows * 2);
+  for (size_t r = 0; r < rows; ++r) {
+    meta[2 * r] = (uint32_t)p.dst[r] | ((uint32_t)p.cnt[r] << 16);
+    meta[2 * r + 1] = (uint32_t)(p.off[r / 32] * 32 + (int)(r % 32));
+  }
+  d.meta = (const uint2 *)put(meta.data(), rows * 8);
+  std::vector<int32_t> lv;
+  for (int q = 0, ps = 0; q < p.npass; ++q)
+    if (p.sync[q]) {
+      lv.push_back(ps);
+      lv.push_back(q);
+      ps = q + 1;
+    }
+  d.nlev = (int)lv.size() / 2;
+  d.lvl = (const int2 *)put(lv.data(), lv.size() * 4);
   return d;
+}
+
+// Cut the high-order programs into chunks of whole passes (≤ chunk_cap bytes unless
+// one pass is larger) in execution order: curl, slift[0..3], strace[0..3].
+dgm_status build_stream(dgm_ctx *c, const HostProgSet &hs, size_t chunk_cap) {
+  const HostProg *progs[9] = {&hs.curl,          &hs.slift[0].prog,  &hs.slift[1].prog,
+                              &hs.slift[2].prog, &hs.slift[3].prog,  &hs.strace[0].prog,
+                              &hs.strace[1].prog, &hs.strace[2].prog, &hs.strace[3].prog};
+  std::vector<char> blob;
+  std::vector<dgm::StreamChunk> ch;
+  dgm::DevStream ds{};
+  size_t maxb = 0;
+  for (int pi = 0; pi < 9; ++pi) {
+    const HostProg &hp = *progs[pi];
+    ds.first[pi] = (int)ch.size();
+    int q = 0;
+    while (q < hp.npass) {
+      const int qa = q;
+      size_t tb = 0;
+      while (q < hp.npass) {
+        const size_t w = (size_t)(hp.off[q + 1] - hp.off[q]);
+        const size_t nb = 256 * (size_t)(q - qa + 1) + 512 * (tb + w);
+        if (q > qa && nb > chunk_cap) break;
+        tb += w;
+        ++q;
+      }
+      const int np = q - qa;
+      const size_t bytes = 256 * (size_t)np + 512 * tb;
+      dgm::StreamChunk sc{(uint32_t)blob.size(), (uint32_t)bytes, np, 0};
+      blob.resize(blob.size() + bytes);
+      uint32_t *meta = (uint32_t *)(blob.data() + sc.off);
+      double *terms = (double *)(blob.data() + sc.off + 256 * (size_t)np);
+      size_t base = 0;
+      for (int qq = qa; qq < q; ++qq) {
+        const int w = hp.off[qq + 1] - hp.off[qq];
+        // padded terms (t >= cnt) keep coef 0 but read a slot some real term of this
+        // pass reads, so they never touch an unwritten (possibly non-finite) slot
+        long long fallback = 0;
+        for (int l = 0; l < 32; ++l)
+          if (hp.dst[(size_t)qq * 32 + l] != 0xFFFF && hp.cnt[(size_t)qq * 32 + l] > 0) {
+            fallback = hp.src[(size_t)hp.off[qq] * 32 + l];
+            break;
+          }
+        for (int l = 0; l < 32; ++l) {
+          const size_t r = (size_t)qq * 32 + l;
+          meta[2 * ((qq - qa) * 32 + l)] =
+              (uint32_t)hp.dst[r] | ((uint32_t)w << 16) | (hp.sync[qq] ? 0x80000000u : 0u);   // uniform pass width
+          meta[2 * ((qq - qa) * 32 + l) + 1] = (uint32_t)(base + l);
+          for (int t = 0; t < w; ++t) {
+            const size_t gi = ((size_t)hp.off[qq] + t) * 32 + l;
+            const size_t li = base + (size_t)t * 32 + l;
+            const bool real = hp.dst[r] != 0xFFFF && t < hp.cnt[r];
+            terms[2 * li] = real ? hp.coef[gi] : 0.0;
+            long long sv = real ? (long long)hp.src[gi] : fallback;
+            std::memcpy(&terms[2 * li + 1], &sv, 8);
+          }
+        }
+        base += (size_t)w * 32;
+      }
+      ch.push_back(sc);
+      if (bytes > maxb) maxb = bytes;
+    }
+    ds.count[pi] = (int)ch.size() - ds.first[pi];
+  }
+  ds.nchunk = (int)ch.size();
+  ds.max_bytes = (int)((maxb + 127) & ~size_t(127));
+  const size_t cb = (ch.size() * sizeof(dgm::StreamChunk) + 255) & ~size_t(255);
+  CUDA_TRY(c, cudaMalloc(&c->d_stream, cb + blob.size()));
+  CUDA_TRY(c, cudaMemcpy(c->d_stream, ch.data(), ch.size() * sizeof(dgm::StreamChunk), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy((char *)c->d_stream + cb, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  ds.chunks = (const dgm::StreamChunk *)c->d_stream;
+  ds.base = (const char *)c->d_stream + cb;
+  c->stream = ds;
+  return DGM_OK;
+}
+
+// ---- dense engine: assemble the operator matrices from the exact programs ------
+// Scalar executor of an ELL program (passes in order respect the DAG levels).
+void exec_prog_host(const HostProg &hp, std::vector<double> &s) {
+  for (int q = 0; q < hp.npass; ++q)
+    for (int l = 0; l < 32; ++l) {
+      const size_t r = (size_t)q * 32 + l;
+      if (hp.dst[r] == 0xFFFF) continue;
+      double acc = 0.0;
+      for (int t = 0; t < hp.cnt[r]; ++t) {
+        const size_t gi = ((size_t)hp.off[q] + t) * 32 + l;
+        acc += hp.coef[gi] * s[hp.src[gi]];
+      }
+      s[hp.dst[r]] = acc;
+    }
+}
+// Staged program: the first level reads in[], later levels the scratch; returns the
+// value of output i (0 when the output has no slot).
+void exec_staged_host(const dgm::HostSProg &sp, const std::vector<double> &in, std::vector<double> &scr,
+                      std::vector<double> &out, int nout) {
+  const HostProg &hp = sp.prog;
+  scr.assign(sp.n_scr + 1, 0.0);
+  bool first = true;
+  for (int q = 0; q < hp.npass; ++q) {
+    for (int l = 0; l < 32; ++l) {
+      const size_t r = (size_t)q * 32 + l;
+      if (hp.dst[r] == 0xFFFF) continue;
+      double acc = 0.0;
+      for (int t = 0; t < hp.cnt[r]; ++t) {
+        const size_t gi = ((size_t)hp.off[q] + t) * 32 + l;
+        acc += hp.coef[gi] * (first ? in[hp.src[gi]] : scr[hp.src[gi]]);
+      }
+      scr[hp.dst[r]] = acc;
+    }
+    if (hp.sync[q]) first = false;
+  }
+  out.assign(nout, 0.0);
+  for (int i = 0; i < nout; ++i) out[i] = sp.out[i] == 0xFFFF ? 0.0 : scr[sp.out[i]];
+}
+
+dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
+  constexpr int BK = 16, BN = 96;
+  static const double T1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
+  static const double T2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
+  const int N = c->N, NF = c->NF;
+  const int Nk = (N + BK - 1) / BK * BK, NFk = (NF + BK - 1) / BK * BK, Np = (N + 31) / 32 * 32;
+  const int k1a = 3 * Nk;
+  const int K1 = k1a + 8 * NFk;
+  const int K2 = 3 * Nk;
+  const int nc1 = 3 * Np;
+  const int nc2 = (8 * NF + BN - 1) / BN * BN;
+  std::vector<double> B1((size_t)K1 * nc1, 0.0), B2((size_t)K2 * nc2, 0.0);
+  // curl: column (c, β) of Ĉ by running the sweep program on that unit input
+  int maxslot = 0;
+  for (int r = 0; r < hs.curl.npass * 32; ++r)
+    if (hs.curl.dst[r] != 0xFFFF && hs.curl.dst[r] > maxslot) maxslot = hs.curl.dst[r];
+  std::vector<double> sl(std::max(maxslot + 1, 12 * N));
+  for (int k = 0; k < 3 * N; ++k) {
+    std::fill(sl.begin(), sl.end(), 0.0);
+    sl[k] = 1.0;
+    exec_prog_host(hs.curl, sl);
+    const size_t row = (size_t)(k / N) * Nk + k % N;
+    for (int m = 0; m < 3; ++m)
+      for (int b = 0; b < N; ++b) B1[row * nc1 + (size_t)m * Np + b] = sl[(size_t)hs.acc + m * N + b];
+  }
+  // lift: L_f e_γ, spread to the components with t̂1 (A) / t̂2 (B)
+  std::vector<double> in, scr, out;
+  for (int f = 0; f < 4; ++f)
+    for (int g = 0; g < NF; ++g) {
+      in.assign(NF, 0.0);
+      in[g] = 1.0;
+      exec_staged_host(hs.slift[f], in, scr, out, N);
+      const size_t ra = (size_t)k1a + (2 * f) * NFk + g, rb = (size_t)k1a + (2 * f + 1) * NFk + g;
+      for (int m = 0; m < 3; ++m)
+        for (int b = 0; b < N; ++b) {
+          B1[ra * nc1 + (size_t)m * Np + b] = T1[f][m] * out[b];
+          B1[rb * nc1 + (size_t)m * Np + b] = T2[f][m] * out[b];
+        }
+    }
+  // traces: R_f e_β, tangential weights t̂1 / t̂2 per component
+  for (int f = 0; f < 4; ++f)
+    for (int b = 0; b < N; ++b) {
+      in.assign(N, 0.0);
+      in[b] = 1.0;
+      exec_staged_host(hs.strace[f], in, scr, out, NF);
+      for (int cc = 0; cc < 3; ++cc)
+        for (int g = 0; g < NF; ++g) {
+          B2[(size_t)(cc * Nk + b) * nc2 + (2 * f) * NF + g] = T1[f][cc] * out[g];
+          B2[(size_t)(cc * Nk + b) * nc2 + (2 * f + 1) * NF + g] = T2[f][cc] * out[g];
+        }
+    }
+  // Entries that are exactly zero in the exact operator can come out as rounding
+  // residue (~1e-17) of cancelling recurrence terms; clear them so the tile masks see
+  // the true sparsity (changes results by < 1e-14 relative).
+  auto clean = [](std::vector<double> &B) {
+    double mx = 0.0;
+    for (double v : B) mx = std::max(mx, std::fabs(v));
+    for (double &v : B)
+      if (std::fabs(v) <= 1e-13 * mx) v = 0.0;
+  };
+  clean(B1);
+  clean(B2);
+  // A-operand column offsets (element stride applied in the kernel); -1 = zero row
+  const int64_t cs = c->n_tet * c->LD;
+  std::vector<int64_t> ko1(K1, -1), ko2(K2, -1);
+  for (int cc = 0; cc < 3; ++cc)
+    for (int b = 0; b < N; ++b) ko1[cc * Nk + b] = ko2[cc * Nk + b] = (int64_t)cc * cs + b;
+  for (int jj = 0; jj < 8; ++jj)
+    for (int g = 0; g < NF; ++g) ko1[k1a + jj * NFk + g] = (int64_t)jj * NF + g;
+  // per n-tile: non-zero k-tiles with the mask of non-zero 16x32 column blocks
+  // (one per warp column of the GEMM CTA)
+  constexpr int GW = 32;
+  auto tiles = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int klo, int khi,
+                   std::vector<uint32_t> &ktl, std::vector<int32_t> &ktoff) {
+    ktl.clear();
+    ktoff.assign(1, 0);
+    for (int t = 0; t < ntn; ++t) {
+      for (int kt = klo / BK; kt < khi / BK; ++kt) {
+        uint32_t mask = 0;
+        for (int grp = 0; grp < BN / GW; ++grp)
+          for (int cc = 0; cc < GW && !(mask >> grp & 1); ++cc) {
+            const int tc = grp * GW + cc;
+            const int col = gather ? (tc / 32) * Np + 32 * t + tc % 32 : t * BN + tc;
+            for (int k = kt * BK; k < (kt + 1) * BK; ++k)
+              if (B[(size_t)k * nc + col] != 0.0) {
+                mask |= 1u << grp;
+                break;
+              }
+          }
+        if (mask) ktl.push_back((uint32_t)kt | (mask << 16));
+      }
+      ktoff.push_back((int32_t)ktl.size());
+    }
+  };
+  std::vector<uint32_t> l1[4], l2;
+  std::vector<int32_t> o1[4], o2;
+  tiles(B1, nc1, Np / 32, true, 0, k1a, l1[1], o1[1]);
+  tiles(B1, nc1, Np / 32, true, k1a, K1, l1[2], o1[2]);
+  tiles(B1, nc1, Np / 32, true, 0, K1, l1[3], o1[3]);
+  tiles(B2, nc2, nc2 / BN, false, 0, K2, l2, o2);
+  if (std::getenv("DGM_DEBUG_DENSE")) {
+    auto bits = [](const std::vector<uint32_t> &l) {
+      long n = 0;
+      for (uint32_t v : l) n += __builtin_popcount(v >> 16);
+      return n;
+    };
+    std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x32)\n", c->p,
+                 l1[3].size(), bits(l1[3]), l2.size(), bits(l2));
+  }
+  // one device allocation
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t bytes = al(B1.size() * 8) + al(B2.size() * 8) + al((size_t)K1 * 8) + al((size_t)K2 * 8) +
+                 al(l2.size() * 4 + 4) + al(o2.size() * 4);
+  for (int i = 1; i < 4; ++i) bytes += al(l1[i].size() * 4 + 4) + al(o1[i].size() * 4);
+  CUDA_TRY(c, cudaMalloc(&c->d_dense, bytes));
+  char *base = (char *)c->d_dense;
+  size_t off = 0;
+  auto put = [&](const void *src, size_t b) -> char * {
+    char *d = base + off;
+    if (b) {
+      cudaError_t e = cudaMemcpy(d, src, b, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return nullptr;
+    }
+    off += al(b + (b == 0 ? 2 : 0));
+    return d;
+  };
+  dgm::DenseOps &D = c->dense;
+  D.B1 = (double *)put(B1.data(), B1.size() * 8);
+  D.B2 = (double *)put(B2.data(), B2.size() * 8);
+  D.koff1 = (int64_t *)put(ko1.data(), ko1.size() * 8);
+  D.koff2 = (int64_t *)put(ko2.data(), ko2.size() * 8);
+  for (int i = 1; i < 4; ++i) {
+    D.ktl1[i] = (uint32_t *)put(l1[i].data(), l1[i].size() * 4);
+    D.ktoff1[i] = (int32_t *)put(o1[i].data(), o1[i].size() * 4);
+  }
+  D.ktl2 = (uint32_t *)put(l2.data(), l2.size() * 4);
+  D.ktoff2 = (int32_t *)put(o2.data(), o2.size() * 4);
+  if (!D.B1 || !D.B2 || !D.ktoff2) return dgm::set_err(c, DGM_ECUDA, "dense_build: upload failed");
+  D.nc1 = nc1;
+  D.nc2 = nc2;
+  D.k1a = k1a;
+  CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NF * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
+  return DGM_OK;
 }
 
 void free_ctx(dgm_ctx *c) {
   if (!c) return;
+  cudaFree(c->d_dense);
+  cudaFree(c->dense.AB);
+  cudaFree(c->d_stream);
   cudaFree(c->d_geo);
   cudaFree(c->d_nbr);
   cudaFree(c->d_nbrf);
@@ -110,7 +389,8 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   if (order < 1 || order > DGM_PMAX)
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
-  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0};
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO};
+  if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_DENSE) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
   if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
     return dgm::set_err(c, DGM_EINVAL, "unknown flux");
   const int p = order;
@@ -121,6 +401,10 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   c->LD = (c->N + 3) & ~3;
   c->n_tet = n;
   c->flux = o.flux;
+  // engine: explicit option, else DGM_ENGINE, else by order (dense measured faster for p >= 6)
+  c->engine = o.engine == DGM_ENGINE_DENSE ? 1 : o.engine == DGM_ENGINE_SPARSE ? 0 : (p >= 6 ? 1 : 0);
+  if (o.engine == DGM_ENGINE_AUTO)
+    if (const char *v = std::getenv("DGM_ENGINE")) c->engine = std::strcmp(v, "dense") == 0 ? 1 : 0;
   auto rep = [&](int32_t v) -> int64_t { return m->rep ? (int64_t)m->rep[v] : (int64_t)v; };
 
   // ---- validate vertex ids and canonical (ascending-rep) order
@@ -308,6 +592,7 @@ dgm_status upload_impl(dgm_ctx *c) {
   int dev = 0;
   CUDA_TRY(c, cudaGetDevice(&dev));
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
+  if (const char *v = std::getenv("DGM_HO_STREAM")) c->ho_stream = std::atoi(v) != 0;
   CUDA_TRY(c, cudaMalloc(&c->d_geo, sizeof(Geo) * n));
   CUDA_TRY(c, cudaMemcpy(c->d_geo, c->h_geo.data(), sizeof(Geo) * n, cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMalloc(&c->d_nbr, 4 * sizeof(int32_t) * n));
@@ -372,6 +657,16 @@ dgm_status upload_impl(dgm_ctx *c) {
   c->progs.norms = (const double *)(base + off);
   off += ((size_t)c->N * 8 + 255) & ~size_t(255);
   CUDA_TRY(c, cudaMemcpy(c->d_blob, buf.data(), bytes, cudaMemcpyHostToDevice));
+  if (c->engine == 1) {
+    dgm_status r = dense_build(c, hs);
+    if (r != DGM_OK) return r;
+  }
+  if (p > dgm::kLanePmax) {
+    const char *v = std::getenv("DGM_ST_CHUNK");
+    const size_t cap = v && *v ? (size_t)std::atol(v) : 16384;
+    dgm_status r = build_stream(c, hs, cap);
+    if (r != DGM_OK) return r;
+  }
   return DGM_OK;
 }
 
@@ -645,6 +940,8 @@ dgm_status dgm_tables(const dgm_ctx *c, int32_t *nbr, int8_t *nbr_face, int8_t *
   if (bc) std::memcpy(bc, c->bc.data(), n);
   return DGM_OK;
 }
+
+int dgm_engine(const dgm_ctx *c) { return c ? (c->engine == 1 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE) : -1; }
 
 int64_t dgm_last_launches(const dgm_ctx *c) { return c ? c->launches : 0; }
 

@@ -47,12 +47,49 @@ struct DevProg {
   const uint8_t *__restrict__ sync;
   // the same terms packed as 16-byte {coef, src} pairs: one 128-bit load per term
   const double2 *__restrict__ term;
+  // per row {dst | cnt << 16, first term index (off*32 + lane)}: one 64-bit load per row
+  const uint2 *__restrict__ meta;
+  // per DAG level {first pass, last pass}
+  const int2 *__restrict__ lvl;
+  int nlev;
 };
 struct DevSProg {
   DevProg prog;
   int n_in, n_scr;
   const uint16_t *__restrict__ out;
 };
+// Table stream for the high-order streamed kernels (dgm_stream.cu): the programs
+// curl, slift[0..3], strace[0..3] cut into chunks of whole passes; each chunk is
+// [meta: npass*32 uint2 {dst | cnt<<16 | level_end<<31, first term (chunk-relative)}]
+// [terms: double2 {coef, src}], copied into shared memory by one bulk TMA copy.
+struct StreamChunk {
+  uint32_t off, bytes;
+  int32_t npass, pad;
+};
+struct DevStream {
+  const char *__restrict__ base;
+  const StreamChunk *__restrict__ chunks;
+  int first[9], count[9];
+  int nchunk, max_bytes;
+};
+
+// Dense-contraction engine (dgm_dense.cu): per-context operator matrices assembled
+// from the exact programs.  Rows are component-blocked and padded to the k-tile
+// (Nk = N, NFk = NF rounded up to 16).  B1 [3Nk+8NFk][3Np]: rows c*Nk+β (curl input),
+// k1a + j*NFk + γ (face field j = f*2+{A,B}); columns m*Np+β (Np = N rounded up to
+// 32).  B2 [3Nk][nc2]: rows c*Nk+β, columns (f*2+k)*NF+γ (trace-buffer order).
+// ktl/ktoff: per n-tile the non-zero k-tiles with a 12-bit mask of non-zero 16x8
+// column groups (sel 1 curl only, 2 flux only, 3 both).
+struct DenseOps {
+  double *B1 = nullptr, *B2 = nullptr, *AB = nullptr;
+  int64_t *koff1 = nullptr, *koff2 = nullptr;
+  int nc1 = 0, nc2 = 0, k1a = 0;
+  uint32_t *ktl1[4] = {nullptr, nullptr, nullptr, nullptr};
+  int32_t *ktoff1[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t *ktl2 = nullptr;
+  int32_t *ktoff2 = nullptr;
+};
+
 struct DevProgs {
   DevProg curl;
   DevProg trace[4];
@@ -95,6 +132,12 @@ struct dgm_ctx {
   int64_t n_tet = 0;
   int flux = 0;
   int sms = 0;
+  int ho_stream = 1;   // sparse, p > kLanePmax: streamed-table kernels (DGM_HO_STREAM=0: one-element CTA kernels)
+  int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
+  dgm::DenseOps dense{};
+  void *d_dense = nullptr;
+  dgm::DevStream stream{};
+  void *d_stream = nullptr;
   std::vector<int32_t> nbr;
   std::vector<int8_t> nbrf, sign, bc;
   std::vector<dgm::Geo> h_geo;
@@ -144,6 +187,16 @@ dgm_status launch_face_energy(dgm_ctx *c, const double *HF, double *out, cudaStr
 dgm_status launch_massdot(dgm_ctx *c, const double *A, const double *B, int use_mu, double *out, cudaStream_t st);
 dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaStream_t st);
 dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
+// dense-contraction engine (dgm_dense.cu), all orders
+dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
+dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
+// trace buffers use the 16-element interleaved layout only on the sparse lane path
+inline bool lane_layout(const dgm_ctx *c);
+
+// streamed-table high-order path (dgm_stream.cu), p > kLanePmax
+dgm_status launch_stream_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
+dgm_status launch_stream_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
+
 // lane-per-element path (dgm_lane.cu), p <= kLanePmax
 constexpr int kLanePmax = 6;
 dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
@@ -151,3 +204,5 @@ dgm_status launch_lane_stage(dgm_ctx *c, int stage, const double *Y, double *X, 
                              cudaStream_t st);
 dgm_status launch_lane_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
 }  // namespace dgm
+
+inline bool dgm::lane_layout(const dgm_ctx *c) { return c->engine == 0 && c->p <= dgm::kLanePmax; }

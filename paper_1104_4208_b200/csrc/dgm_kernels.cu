@@ -493,7 +493,7 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
                            int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
                            cudaStream_t st) {
   if (c->n_tet == 0) return DGM_OK;
-  if (c->p <= kLanePmax)
+  if (c->engine == 0 && c->p <= kLanePmax)
     return launch_lane_stage(c, stage, Y, X, dX, dt, do_curl, do_flux, out_mode, trY, trX, trOut, st);
   StageArgs a;
   a.Y = Y;
@@ -513,12 +513,16 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
   a.do_curl = do_curl;
   a.do_flux = do_flux;
   a.out_mode = out_mode;
+  if (c->engine == 1) return launch_dense_stage(c, a, trY, trOut, st);
+  if (c->ho_stream) return launch_stream_stage(c, a, trY, trOut, st);
   DGM_DISPATCH_HI(c->p, launch_stage2_p, c, a, trY, trOut, st)
 }
 
 dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
   if (c->n_tet == 0) return DGM_OK;
+  if (c->engine == 1) return launch_dense_traces(c, X, tr, st);
   if (c->p <= kLanePmax) return launch_lane_traces(c, X, tr, st);
+  if (c->ho_stream) return launch_stream_traces(c, X, tr, st);
   DGM_DISPATCH_HI(c->p, launch_trace2_p, c, X, tr, st)
 }
 
@@ -655,7 +659,7 @@ dgm_status launch_hf(dgm_ctx *c, const double *TE, double *HF, double *dHF, doub
   int64_t grid = (total + 255) / 256;
   if (grid > 8 * (int64_t)c->sms) grid = 8 * (int64_t)c->sms;
   hf_kernel<<<(unsigned)grid, 256, 0, st>>>(TE, HF, dHF, dt, c->d_fside, c->d_sign, c->d_fgeo, c->n_faces, c->NF,
-                                            c->p <= kLanePmax ? 1 : 0);
+                                            lane_layout(c) ? 1 : 0);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("hf_kernel: ") + cudaGetErrorString(e));

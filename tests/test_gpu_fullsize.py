@@ -25,7 +25,7 @@ def _cuda():
     assert torch.cuda.is_available(), "GPU tests need CUDA (no CPU fallback exists)"
 
 
-def _setup(name):
+def _setup(name, engine="auto"):
     import torch
     from paper_1104_4208_b200 import Context
     cfg = di.CONFIGS[name]
@@ -33,7 +33,7 @@ def _setup(name):
     eps, mu = di.config_materials(name, m.n_tet)
     rep = m.rep if any(cfg["periodic"]) else None
     p = cfg["p"]
-    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=cfg["flux"])
+    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=cfg["flux"], engine=engine)
     deg = torch.as_tensor(di.mode_degrees(p), dtype=torch.float64, device="cuda")
     scale = 1.0 / (1.0 + deg) ** 2
     g = torch.Generator(device="cuda").manual_seed(3000 + di.config_index(name))
@@ -69,9 +69,10 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
+@pytest.mark.parametrize("engine", ["sparse", "dense"])
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
-def test_fullsize_apply_sampled(name):
-    cfg, m, c, Ed, Hd, B = _setup(name)
+def test_fullsize_apply_sampled(name, engine):
+    cfg, m, c, Ed, Hd, B = _setup(name, engine)
     dE, dH = c.empty_field(), c.empty_field()
     c.dgm_apply_curl(Ed, Hd, dE, dH)
     c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
@@ -84,10 +85,11 @@ def test_fullsize_apply_sampled(name):
     assert _rel(dH[:, t, :c.N].cpu().numpy(), ref["dH"]) <= TOL
 
 
+@pytest.mark.parametrize("engine", ["sparse", "dense"])
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
-def test_fullsize_one_step_sampled(name):
+def test_fullsize_one_step_sampled(name, engine):
     from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
-    cfg, m, c, Ed, Hd, B = _setup(name)
+    cfg, m, c, Ed, Hd, B = _setup(name, engine)
     S = SubsetEval(B)
     el = _sample(B, 64, 11)
     get0 = _getter(c, Ed.clone(), Hd.clone())

@@ -41,9 +41,14 @@ def _problem(n, periodic, p, flux, seed=7, materials=True, jitter=0.1):
     return m, rep, eps, mu
 
 
-def _ctx(m, rep, p, eps, mu, flux):
+ENGINES = ["sparse", "dense"]   # the paper's recurrences / the dense DMMA contractions (include/dgm.h)
+
+
+def _ctx(m, rep, p, eps, mu, flux, engine="auto"):
     from paper_1104_4208_b200 import Context
-    return Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=flux)
+    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=flux, engine=engine)
+    assert engine == "auto" or c.engine == engine
+    return c
 
 
 CASES = {
@@ -64,11 +69,11 @@ def test_tables_bit_exact(case):
         assert got.dtype == want.dtype and np.array_equal(got, want)
 
 
-def _apply_parity(case, p):
+def _apply_parity(case, p, engine):
     periodic, flux, n = CASES[case]
     m, rep, eps, mu = _problem(n, periodic, p, flux)
     B = TierB(m.xyz, m.tet, rep, p, eps, mu, flux)
-    c = _ctx(m, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux, engine)
     rng = np.random.default_rng(p)
     E = rng.standard_normal((3, m.n_tet, B.N))
     H = rng.standard_normal((3, m.n_tet, B.N))
@@ -87,26 +92,29 @@ def _apply_parity(case, p):
     return errs
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("p", list(range(1, 11)))
-def test_apply_parity_all_orders(p):
-    errs = _apply_parity("pec-central", p)
+def test_apply_parity_all_orders(p, engine):
+    errs = _apply_parity("pec-central", p, engine)
     assert max(errs.values()) <= TOL_APPLY, errs
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("case", ["periodic-central", "pec-upwind", "mixed-upwind"])
 @pytest.mark.parametrize("p", [2, 5, 8, 10])
-def test_apply_parity_cases(case, p):
-    errs = _apply_parity(case, p)
+def test_apply_parity_cases(case, p, engine):
+    errs = _apply_parity(case, p, engine)
     assert max(errs.values()) <= TOL_APPLY, errs
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("p", [2, 4, 6])
-def test_step_parity_100(case, p):
+@pytest.mark.parametrize("p", [2, 4, 6, 9])
+def test_step_parity_100(case, p, engine):
     periodic, flux, n = CASES[case]
     m, rep, eps, mu = _problem(n, periodic, p, flux)
     B = TierB(m.xyz, m.tet, rep, p, eps, mu, flux)
-    c = _ctx(m, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux, engine)
     rng = np.random.default_rng(10 + p)
     E = rng.standard_normal((3, m.n_tet, B.N)) / (1 + np.arange(B.N)) ** 0.5
     H = rng.standard_normal((3, m.n_tet, B.N)) / (1 + np.arange(B.N)) ** 0.5
@@ -158,7 +166,8 @@ def test_config_c1_vs_tier_a():
     assert np.abs(c.to_host(Ed) - fields.project(m.xyz, m.tet, p, Ee)).max() < 0.05
 
 
-def test_config_c2_full_100_steps():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config_c2_full_100_steps(engine):
     """C2 at full size: 16³ Kuhn periodic (24,576 tets), p=4, plane wave + noise,
     central, 100 steps, against tier B."""
     cfg = di.CONFIGS["C2"]
@@ -171,7 +180,7 @@ def test_config_c2_full_100_steps():
     rng = np.random.default_rng(3000 + 2)
     E = fields.project(m.xyz, m.tet, p, E0) + 1e-3 * rng.standard_normal((3, m.n_tet, B.N))
     H = fields.project(m.xyz, m.tet, p, Hh) + 1e-3 * rng.standard_normal((3, m.n_tet, B.N))
-    c = _ctx(m, m.rep, p, 1.0, 1.0, "central")
+    c = _ctx(m, m.rep, p, 1.0, 1.0, "central", engine)
     Ed, Hd = c.to_device(E), c.to_device(H)
     c.dgm_step(Ed, Hd, dt, cfg["steps"])
     Er, Hr, _ = symplectic_euler(B, E, H, dt, cfg["steps"])
@@ -190,16 +199,18 @@ def test_bad_inputs_fail_loudly():
         Context(m.xyz, m.tet, 2, eps=-1.0)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("case", ["pec-central", "mixed-upwind"])
 @pytest.mark.parametrize("p", [3, 7])
-def test_step_continue_matches_single_call(case, p):
+def test_step_continue_matches_single_call(case, p, engine):
     """DGM_STEP_CONTINUE: k calls of 1 step reusing the trace buffers give the
     same bits as one call of k steps; after dgm_apply_flux the buffers are
     invalidated and the call falls back to recomputing them."""
     from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
     periodic, flux, n = CASES[case]
     m, rep, eps, mu = _problem(n, periodic, p, flux)
-    c = _ctx(m, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux, engine)
+    per_step = 2 if engine == "sparse" else 6   # stage kernels / (flux, stage GEMM, trace GEMM) x 2
     rng = np.random.default_rng(p)
     E = rng.standard_normal((3, m.n_tet, c.N))
     H = rng.standard_normal((3, m.n_tet, c.N))
@@ -209,21 +220,22 @@ def test_step_continue_matches_single_call(case, p):
     c.dgm_step(E2, H2, 1e-3, 1)
     for _ in range(4):
         c.dgm_step_ex(E2, H2, 1e-3, 1, DGM_STEP_CONTINUE)
-        assert c.dgm_last_launches() == 2
+        assert c.dgm_last_launches() == per_step
     c.dgm_apply_flux(E2, H2, c.empty_field(), None)     # invalidates the buffers
     c.dgm_step_ex(E2, H2, 1e-3, 1, DGM_STEP_CONTINUE)
-    assert c.dgm_last_launches() > 2
+    assert c.dgm_last_launches() > per_step
     assert bool((E1 == E2).all()) and bool((H1 == H2).all())
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("case,p", [("periodic-central", 4), ("pec-upwind", 3), ("mixed-upwind", 8)])
-def test_step_host_matches_device_step(case, p):
+def test_step_host_matches_device_step(case, p, engine):
     """dgm_step_host (host buffers, overlapped copies on a side stream) gives the
     same bits as dgm_step on device buffers."""
     import torch
     periodic, flux, n = CASES[case]
     m, rep, eps, mu = _problem(n, periodic, p, flux)
-    c = _ctx(m, rep, p, eps, mu, flux)
+    c = _ctx(m, rep, p, eps, mu, flux, engine)
     rng = np.random.default_rng(p + 40)
     E = rng.standard_normal((3, m.n_tet, c.N))
     H = rng.standard_normal((3, m.n_tet, c.N))

@@ -20,14 +20,14 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-def _case(p, periodic, n, seed=5, alpha0=1.0):
+def _case(p, periodic, n, seed=5, alpha0=1.0, engine="auto"):
     import torch
     from paper_1104_4208_b200 import Context
     m = di.kuhn_mesh(n, periodic=periodic, jitter=0.1, seed=seed)
     rep = m.rep if any(periodic) else None
     rng = np.random.default_rng(seed)
     eps, mu = rng.uniform(1, 4, m.n_tet), rng.uniform(1, 2, m.n_tet)
-    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux="stabilized", alpha0=alpha0)
+    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux="stabilized", alpha0=alpha0, engine=engine)
     B = TierBStab(m.xyz, m.tet, rep, p, eps, mu, alpha0=alpha0)
     E = rng.standard_normal((3, m.n_tet, c.N))
     H = rng.standard_normal((3, m.n_tet, c.N))
@@ -47,10 +47,11 @@ CASES = [(p, (False,) * 3, 2) for p in (1, 2, 3, 4, 5, 6, 7, 8)] + \
         [(3, (True,) * 3, 3), (6, (False, True, True), 3), (7, (True, False, True), 3)]
 
 
+@pytest.mark.parametrize("engine", ["sparse", "dense"])
 @pytest.mark.parametrize("p,periodic,n", CASES)
-def test_stab_faces_and_rhs_parity(p, periodic, n):
+def test_stab_faces_and_rhs_parity(p, periodic, n, engine):
     import torch
-    m, c, B, E, H, HF = _case(p, periodic, n)
+    m, c, B, E, H, HF = _case(p, periodic, n, engine=engine)
     nf, fid = c.dgm_faces()
     assert nf == B.n_faces
     assert np.array_equal(fid, B.fid)
@@ -66,12 +67,13 @@ def test_stab_faces_and_rhs_parity(p, periodic, n):
     assert w == pytest.approx(B.energy(E, H, HF), rel=1e-12)
 
 
+@pytest.mark.parametrize("engine", ["sparse", "dense"])
 @pytest.mark.parametrize("p,periodic,n", [(2, (False,) * 3, 2), (4, (True,) * 3, 3), (7, (False,) * 3, 2)])
-def test_stab_steps_parity_and_energy(p, periodic, n):
+def test_stab_steps_parity_and_energy(p, periodic, n, engine):
     """100 symplectic-Euler steps with (H, H^F) advanced together vs the oracle
     (≤1e-10), then the discrete energy stays bounded (leapfrog on a skew system)."""
     import torch
-    m, c, B, E, H, HF = _case(p, periodic, n, seed=7, alpha0=2.0)
+    m, c, B, E, H, HF = _case(p, periodic, n, seed=7, alpha0=2.0, engine=engine)
     Ed, Hd = _dev(c, E), _dev(c, H)
     HFd = torch.as_tensor(HF, device="cuda").contiguous()
     rho = c.dgm_spectral_radius(iters=60)
