@@ -31,16 +31,18 @@ namespace dgm {
 namespace {
 
 constexpr int BN = 96, BK = 16;
-constexpr int WM = 32, WN = 32;   // warp tile: 4 x 4 MMAs of 8x8; the 3 warp columns = the 3 column blocks
-constexpr int BST = BN + 4;       // padded smem strides (conflict-free fragment loads)
+constexpr int WM = 16;             // warp tile: 16 rows x all 96 columns (2 x 12 MMAs of 8x8)
+constexpr int BST = BN + 4;        // padded smem strides (conflict-free fragment loads)
+constexpr int AKS = BK + 4;        // A tile row stride ([m][k] layout)
 
-// CTA shape: BM elements x BN columns, (BM/32) x 2 warps, NST-stage cp.async pipeline
+// CTA shape: BM elements x BN columns; the BM/16 warps split the elements only, so
+// every warp sees the same operator block mask (no intra-CTA imbalance).
 template <int BM_, int NST_>
 struct Cfg {
-  static constexpr int BM = BM_, NSTAGE = NST_, AST = BM_ + 4, NTHREADS = (BM_ / WM) * (BN / WN) * 32;
-  static constexpr int MINB = BM_ == 64 ? (NST_ <= 3 ? 3 : 2) : 1;
+  static constexpr int BM = BM_, NSTAGE = NST_, NTHREADS = (BM_ / WM) * 32;
+  static constexpr int MINB = BM_ == 32 ? 4 : (BM_ == 64 ? 3 : 1);
   struct Smem {
-    double A[NST_][BK][AST];
+    double A[NST_][BM_][AKS];
     double B[NST_][BK][BST];
   };
   static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * BST + BM_ * 8);   // C tile + geometry rows
@@ -50,9 +52,10 @@ struct Cfg {
 enum { EPI_STAGE = 0, EPI_TRACE = 1 };
 
 struct GemmArgs {
-  // A operand, element e, column k (component-blocked rows, see DenseOps):
-  //   k <  k1: c = k / Nk, β = k % Nk  -> p0 + e*ld0 + c*cs + β      (β < N, else 0)
-  //   k >= k1: j = (k-k1) / NFk, γ = ..  -> p1 + e*ld1 + j*NF + γ     (γ < NF, j < 8, else 0)
+  // A operand, element e, column k (component-blocked rows, see DenseOps; every
+  // 16-row k-tile lies inside one block):
+  //   k <  k1: c = k / Nk, β = k % Nk  -> p0 + e*ld0 + c*cs + β       (β < N, else 0)
+  //   k >= k1: j = (k-k1) / NFk, γ = ..  -> p1 + e*ld1 + j*NFk + γ    (γ < NF, else 0)
   const double *p0, *p1;
   int64_t ld0, ld1, cs;
   int k1, Nk, NFk;
@@ -60,7 +63,7 @@ struct GemmArgs {
   const double *Bm;
   int NC;
   int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t gathers β in [32t, 32t+32)
-  const uint32_t *ktl;     // per non-zero k-tile: kt | (12-bit mask of non-zero 16x8 column groups) << 16
+  const uint32_t *ktl;     // per non-zero k-tile: kt | (3-bit mask of non-zero 16x32 column blocks) << 16
   const int32_t *ktoff;
   int ntiles_n;
   int64_t n_tet;
@@ -69,14 +72,14 @@ struct GemmArgs {
   int ncols;   // valid output columns (EPI_TRACE: 8NF)
   const Geo *geo;
   double *X, *dX, *tr;
-  const double *Xin;   // (unused by the GEMM; kept for symmetry)
   double dt;
   int stageE, out_mode;
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cpa8(double *dst, const double *src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(valid ? 8 : 0));
+// 16-byte async copy, zero-filling beyond `bytes` (0, 8 or 16)
+__device__ __forceinline__ void cpa16z(double *dst, const double *src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(bytes));
 }
 __device__ __forceinline__ void cpa16(double *dst, const double *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src));
@@ -93,28 +96,34 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// load k-tile kt of the A (transposed to [k][m]) and B operands into stage buffer st
+// load k-tile kt of A ([m][k], 16-byte copies of mode pairs) and B into stage st
 template <int EPI, class C>
 __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, int st, int64_t m0, int nt, int kt,
                                           int tid) {
   constexpr int BM = C::BM, NTHREADS = C::NTHREADS;
-  const int kk = tid & (BK - 1);
-  const int k = kt * BK + kk;
-  int64_t ko = -1;
-  const bool lo = k < g.k1;
+  const int k0 = kt * BK;
+  const bool lo = k0 < g.k1;
+  int blk, q0, lim;   // block index, first in-block index of the tile, valid count in the block
   if (lo) {
-    const int c = k / g.Nk, b = k - c * g.Nk;
-    if (b < g.N) ko = c * g.cs + b;
+    blk = k0 / g.Nk;
+    q0 = k0 - blk * g.Nk;
+    lim = g.N;
   } else {
-    const int j = (k - g.k1) / g.NFk, gm = (k - g.k1) - j * g.NFk;
-    if (gm < g.NF && j < 8) ko = (int64_t)j * g.NF + gm;
+    blk = (k0 - g.k1) / g.NFk;
+    q0 = (k0 - g.k1) - blk * g.NFk;
+    lim = g.NF;
   }
-  const double *base = lo ? g.p0 : g.p1;
+  const double *base = lo ? g.p0 + blk * g.cs : g.p1 + (int64_t)blk * g.NFk;
   const int64_t ld = lo ? g.ld0 : g.ld1;
-  for (int m = tid >> 4; m < BM; m += NTHREADS / BK) {
+#pragma unroll
+  for (int i = 0; i < BM * (BK / 2) / NTHREADS; ++i) {
+    const int idx = tid + i * NTHREADS;
+    const int m = idx >> 3, kp = idx & 7;
     const int64_t e = m0 + m;
-    const bool ok = ko >= 0 && e < g.n_tet;
-    cpa8(&sm.A[st][kk][m], ok ? base + e * ld + ko : g.p0, ok);
+    const int q = q0 + 2 * kp;
+    int bytes = q + 1 < lim ? 16 : (q < lim ? 8 : 0);
+    if (e >= g.n_tet) bytes = 0;
+    cpa16z(&sm.A[st][m][2 * kp], bytes ? base + e * ld + q : g.p0, bytes);
   }
   const double *bsrc = g.Bm + (int64_t)kt * BK * g.NC;
 #pragma unroll
@@ -129,11 +138,11 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
 
 template <int EPI, class C>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) {
-  constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS, WMN = BM / WM;
+  constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS;
   extern __shared__ __align__(16) unsigned char dsm[];
   typename C::Smem &sm = *reinterpret_cast<typename C::Smem *>(dsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WMN, wn = warp / WMN;
+  const int wm = warp;
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
   const int64_t mtiles = (g.n_tet + BM - 1) / BM;
   const int64_t ntile_total = mtiles * g.ntiles_n;
@@ -143,11 +152,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     const int n0 = nt * BN;
     const uint32_t *kts = g.ktl + g.ktoff[nt];
     const int nk = g.ktoff[nt + 1] - g.ktoff[nt];
-    double acc[4][4][2];   // [column group j][row group i][pair]
+    double acc[12][2][2];   // [column group j][row group i][pair]
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 12; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
+      for (int i = 0; i < 2; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
@@ -161,20 +170,27 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       if (nx < nk) load_tile<EPI, C>(g, sm, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFFFu), tid);
       cp_commit();
       const int st = it % NSTAGE;
-      // skip this warp's 16x32 operator block when it is zero (warp-uniform branch
-      // around the whole k-tile, so the tensor pipe is not occupied)
-      if ((kts[it] >> (16 + wn)) & 1u) {
+      double a[BK / 4][2];
 #pragma unroll
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
-          double a[4], b[4];
+      for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = sm.A[st][k4 * 4 + gc][wm * WM + i * 8 + gr];
+        for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
+      const unsigned mask = kts[it] >> 16;
+      // skip the zero 16x32 blocks of the operator: a CTA-uniform branch around a
+      // whole column block, so the tensor pipe is not occupied by dead MMAs
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = sm.B[st][k4 * 4 + gc][wn * WN + j * 8 + gr];
+      for (int grp = 0; grp < 3; ++grp) {
+        if (mask & (1u << grp)) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int k4 = 0; k4 < BK / 4; ++k4) {
+            double b[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dmma(acc[j][i][0], acc[j][i][1], a[i], b[j]);
+            for (int jj = 0; jj < 4; ++jj) b[jj] = sm.B[st][k4 * 4 + gc][grp * 32 + jj * 8 + gr];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) dmma(acc[grp * 4 + jj][i][0], acc[grp * 4 + jj][i][1], a[k4][i], b[jj]);
+          }
         }
       }
     }
@@ -183,13 +199,13 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     if (EPI == EPI_TRACE) {
       // C fragment: row gr (+8i), cols 2gc, 2gc+1 (+8j) -> tr[e][col]
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 2; ++i) {
         const int64_t e = m0 + wm * WM + i * 8 + gr;
         if (e >= g.n_tet) continue;
         double *row = g.tr + e * (int64_t)g.ncols;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = n0 + wn * WN + j * 8 + 2 * gc;
+        for (int j = 0; j < 12; ++j) {
+          const int col = n0 + j * 8 + 2 * gc;
           if (col + 1 < g.ncols) {
             *reinterpret_cast<double2 *>(row + col) = make_double2(acc[j][i][0], acc[j][i][1]);
           } else if (col < g.ncols) {
@@ -201,10 +217,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       // stage the tile in shared memory, then per (element, mode): G' mix and update
       double(*Cs)[BST] = reinterpret_cast<double(*)[BST]>(dsm);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int r = wm * WM + i * 8 + gr, c = wn * WN + j * 8 + 2 * gc;
+        for (int j = 0; j < 12; ++j) {
+          const int r = wm * WM + i * 8 + gr, c = j * 8 + 2 * gc;
           Cs[r][c] = acc[j][i][0];
           Cs[r][c + 1] = acc[j][i][1];
         }
@@ -257,7 +273,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
 // A, B face fields of every (element, face, mode) from the trace buffers
 // (tr[e][f][k][γ]); same flux as the stage kernels (reading G1/G2/G17).
 template <bool UP>
-__global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, double *__restrict__ AB, int NF) {
+__global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, double *__restrict__ AB, int NF,
+                                  int NFk) {
   const int64_t total = a.n_tet * 4 * NF;
   const bool stageE = a.stage == STAGE_E;
   const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
@@ -317,9 +334,9 @@ __global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, d
       A += ps * (j1 * M[0] + j2 * M[1]);
       B += ps * (j1 * M[1] + j2 * M[2]);
     }
-    double *o = AB + ef * 2 * NF;
+    double *o = AB + ef * 2 * NFk;   // AB[e][(f*2+{A,B})*NFk + γ]
     o[gm] = A;
-    o[NF + gm] = B;
+    o[NFk + gm] = B;
   }
 }
 
@@ -350,7 +367,7 @@ dgm_status gemm_go(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
   switch (dense_cfg()) {
     case 1: return gemm_go_c<EPI, Cfg<64, 4>>(c, g, st);
     case 2: return gemm_go_c<EPI, Cfg<128, 3>>(c, g, st);
-    case 3: return gemm_go_c<EPI, Cfg<128, 4>>(c, g, st);
+    case 3: return gemm_go_c<EPI, Cfg<32, 4>>(c, g, st);
     default: return gemm_go_c<EPI, Cfg<64, 3>>(c, g, st);
   }
 }
@@ -364,9 +381,9 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     int64_t grid = (total + 255) / 256;
     if (grid > 16 * (int64_t)c->sms) grid = 16 * (int64_t)c->sms;
     if (a.upwind)
-      dense_flux_kernel<true><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF);
+      dense_flux_kernel<true><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF, (c->NF + BK - 1) / BK * BK);
     else
-      dense_flux_kernel<false><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF);
+      dense_flux_kernel<false><<<(unsigned)grid, 256, 0, st>>>(a, trY, D.AB, c->NF, (c->NF + BK - 1) / BK * BK);
     c->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("dense_flux_kernel: ") + cudaGetErrorString(e));
@@ -375,7 +392,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.p0 = a.Y;
   g.p1 = D.AB;
   g.ld0 = c->LD;
-  g.ld1 = 8 * c->NF;
+  g.ld1 = 8 * ((c->NF + BK - 1) / BK * BK);
   g.cs = c->n_tet * c->LD;
   g.k1 = D.k1a;
   g.Nk = D.k1a / 3;

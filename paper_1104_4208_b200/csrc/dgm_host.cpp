@@ -352,7 +352,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   D.nc1 = nc1;
   D.nc2 = nc2;
   D.k1a = k1a;
-  CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NF * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
+  CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NFk * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
   return DGM_OK;
 }
 
