@@ -157,13 +157,28 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     for (int j = 0; j < 12; ++j)
 #pragma unroll
       for (int i = 0; i < 2; ++i) acc[j][i][0] = acc[j][i][1] = 0.0;
+    if (EPI == EPI_STAGE && g.out_mode == OUT_UPDATE) {
+      // pull this tile's X block (64 elements x 3 x 32 modes) into L2 while the k-loop
+      // runs, so the read-modify-write epilogue does not wait on HBM
+      const int64_t cs = g.n_tet * g.LD;
+      for (int q = tid; q < BM * 3; q += NTHREADS) {
+        const int64_t e = m0 + q / 3;
+        if (e < g.n_tet) {
+          const double *px = g.X + (q % 3) * cs + e * g.LD + 32 * nt;
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px));
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px + 16));
+        }
+      }
+    }
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
       if (s < nk) load_tile<EPI, C>(g, sm, s, m0, nt, (int)(kts[s] & 0xFFFFu), tid);
       cp_commit();
     }
+    uint32_t kcur = nk > 0 ? kts[0] : 0u;
     for (int it = 0; it < nk; ++it) {
+      const uint32_t knext = it + 1 < nk ? kts[it + 1] : 0u;   // one ahead: off the critical path
       cp_wait<NSTAGE - 2>();
       __syncthreads();
       const int nx = it + NSTAGE - 1;
@@ -175,7 +190,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
-      const unsigned mask = kts[it] >> 16;
+      const unsigned mask = kcur >> 16;
+      kcur = knext;
       // skip the zero 16x32 blocks of the operator: a CTA-uniform branch around a
       // whole column block, so the tensor pipe is not occupied by dead MMAs
 #pragma unroll
@@ -237,32 +253,39 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       }
       __syncthreads();
       constexpr int MODES = BN / 3;
+      constexpr int U = 4;   // items per batch: their 3U loads are in flight together
       const int64_t cs = g.n_tet * g.LD;
-#pragma unroll 4
-      for (int idx = tid; idx < BM * MODES; idx += NTHREADS) {
-        const int r = idx / MODES, ml = idx - r * MODES;
-        const int64_t e = m0 + r;
-        const int b = 32 * nt + ml;
-        if (e >= g.n_tet || b >= g.N) continue;
-        const double *G = Gs[r];
-        const double cm = G[6];
-        const double v0 = Cs[r][ml], v1 = Cs[r][32 + ml], v2 = Cs[r][64 + ml];
-        const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
-        const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
-        const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
-        const int64_t o = e * g.LD + b;
-        if (g.out_mode == OUT_UPDATE) {
-          g.X[o] += g.dt * x0;
-          g.X[cs + o] += g.dt * x1;
-          g.X[2 * cs + o] += g.dt * x2;
-        } else if (g.out_mode == OUT_WRITE) {
-          g.dX[o] = x0;
-          g.dX[cs + o] = x1;
-          g.dX[2 * cs + o] = x2;
-        } else {
-          g.dX[o] += x0;
-          g.dX[cs + o] += x1;
-          g.dX[2 * cs + o] += x2;
+      const bool upd = g.out_mode == OUT_UPDATE;
+      double *out = upd ? g.X : g.dX;
+      for (int base = tid; base < BM * MODES; base += U * NTHREADS) {
+        int64_t o[U];
+        double xv[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = base + u * NTHREADS;
+          const int r = idx / MODES, ml = idx - r * MODES;
+          const int64_t e = m0 + r;
+          const int b = 32 * nt + ml;
+          o[u] = (idx < BM * MODES && e < g.n_tet && b < g.N) ? e * g.LD + b : -1;
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            xv[u][cc] = (o[u] >= 0 && g.out_mode != OUT_WRITE) ? out[cc * cs + o[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (o[u] < 0) continue;
+          const int idx = base + u * NTHREADS;
+          const int r = idx / MODES, ml = idx - r * MODES;
+          const double *G = Gs[r];
+          const double cm = G[6];
+          const double v0 = Cs[r][ml], v1 = Cs[r][32 + ml], v2 = Cs[r][64 + ml];
+          const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
+          const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
+          const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
+          const double sc = upd ? g.dt : 1.0;
+          out[o[u]] = xv[u][0] + sc * x0;
+          out[cs + o[u]] = xv[u][1] + sc * x1;
+          out[2 * cs + o[u]] = xv[u][2] + sc * x2;
         }
       }
     }
