@@ -30,17 +30,19 @@
 namespace dgm {
 namespace {
 
-constexpr int BN = 96, BK = 16;
-constexpr int WM = 16;             // warp tile: 16 rows x all 96 columns (2 x 12 MMAs of 8x8)
-constexpr int BST = BN + 4;        // padded smem strides (conflict-free fragment loads)
+constexpr int BN = 96, BK = 16;  // BN: one warp column = three 32-column blocks
+constexpr int WM = 16;             // warp tile: 16 rows x 96 columns (2 x 12 MMAs of 8x8)
+constexpr int NH = kDenseNH;       // warp columns per CTA: CTA tile = BM x (96 NH)
+constexpr int BNT = BN * NH;
+constexpr int BST = BNT + 4;       // padded smem strides (conflict-free fragment loads)
 constexpr int AKS = BK + 4;        // A tile row stride ([m][k] layout)
 
-// CTA shape: BM elements x BN columns; the BM/16 warps split the elements only, so
-// every warp sees the same operator block mask (no intra-CTA imbalance).
+// CTA shape: BM elements x BNT columns; (BM/16) x NH warps.  Warps of one warp column
+// see the same operator block mask.
 template <int BM_, int NST_>
 struct Cfg {
-  static constexpr int BM = BM_, NSTAGE = NST_, NTHREADS = (BM_ / WM) * 32;
-  static constexpr int MINB = BM_ == 32 ? 4 : (BM_ == 64 ? 3 : 1);
+  static constexpr int BM = BM_, NSTAGE = NST_, NTHREADS = (BM_ / WM) * NH * 32;
+  static constexpr int MINB = NH == 1 ? (BM_ == 32 ? 4 : (BM_ == 64 ? 3 : 1)) : (BM_ == 64 ? 2 : 1);
   struct Smem {
     double A[NST_][BM_][AKS];
     double B[NST_][BK][BST];
@@ -62,8 +64,9 @@ struct GemmArgs {
   // B operand: [Kpad][NC] row-major; per n-tile the list of non-zero k-tiles
   const double *Bm;
   int NC;
-  int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t gathers β in [32t, 32t+32)
-  const uint32_t *ktl;     // per non-zero k-tile: kt | (3-bit mask of non-zero 16x32 column blocks) << 16
+  int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t, warp column h gathers
+                           // β in [32(NH t + h), +32)
+  const uint32_t *ktl;     // per non-zero k-tile: kt | (3NH-bit mask of non-zero 16x32 column blocks) << 16
   const int32_t *ktoff;
   int ntiles_n;
   int64_t n_tet;
@@ -127,11 +130,13 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
   }
   const double *bsrc = g.Bm + (int64_t)kt * BK * g.NC;
 #pragma unroll
-  for (int i = 0; i < BK * BN / 2 / NTHREADS; ++i) {
+  for (int i = 0; i < BK * BNT / 2 / NTHREADS; ++i) {
     const int idx = tid + i * NTHREADS;
-    const int r = idx / (BN / 2), c2 = idx - r * (BN / 2);
-    // EPI_STAGE gathers the three component blocks of modes [32nt, 32nt+32); traces are contiguous
-    const int col = EPI == EPI_STAGE ? (c2 >> 4) * g.Np + 32 * nt + 2 * (c2 & 15) : nt * BN + 2 * c2;
+    const int r = idx / (BNT / 2), c2 = idx - r * (BNT / 2);
+    // EPI_STAGE: warp column h = c2 / 48 gathers the three component blocks of modes
+    // [32(NH nt + h), +32); traces are contiguous
+    const int h = c2 / (BN / 2), c3 = c2 - h * (BN / 2);
+    const int col = EPI == EPI_STAGE ? (c3 >> 4) * g.Np + 32 * (NH * nt + h) + 2 * (c3 & 15) : nt * BNT + 2 * c2;
     cpa16(&sm.B[st][r][2 * c2], bsrc + (int64_t)r * g.NC + col);
   }
 }
@@ -142,14 +147,14 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
   extern __shared__ __align__(16) unsigned char dsm[];
   typename C::Smem &sm = *reinterpret_cast<typename C::Smem *>(dsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp;
+  const int wm = warp % (BM / WM), wn = warp / (BM / WM);
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
   const int64_t mtiles = (g.n_tet + BM - 1) / BM;
   const int64_t ntile_total = mtiles * g.ntiles_n;
   for (int64_t t = blockIdx.x; t < ntile_total; t += gridDim.x) {
     const int64_t m0 = (t / g.ntiles_n) * BM;
     const int nt = (int)(t % g.ntiles_n);
-    const int n0 = nt * BN;
+    const int n0 = nt * BNT;
     const uint32_t *kts = g.ktl + g.ktoff[nt];
     const int nk = g.ktoff[nt + 1] - g.ktoff[nt];
     double acc[12][2][2];   // [column group j][row group i][pair]
@@ -164,9 +169,9 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int q = tid; q < BM * 3; q += NTHREADS) {
         const int64_t e = m0 + q / 3;
         if (e < g.n_tet) {
-          const double *px = g.X + (q % 3) * cs + e * g.LD + 32 * nt;
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px));
-          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px + 16));
+          const double *px = g.X + (q % 3) * cs + e * g.LD + 32 * NH * nt;
+#pragma unroll
+          for (int l = 0; l < 2 * NH; ++l) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px + 16 * l));
         }
       }
     }
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
-      const unsigned mask = kcur >> 16;
+      const unsigned mask = (kcur >> (16 + 3 * wn)) & 7u;
       kcur = knext;
       // skip the zero 16x32 blocks of the operator: a CTA-uniform branch around a
       // whole column block, so the tensor pipe is not occupied by dead MMAs
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           for (int k4 = 0; k4 < BK / 4; ++k4) {
             double b[4];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) b[jj] = sm.B[st][k4 * 4 + gc][grp * 32 + jj * 8 + gr];
+            for (int jj = 0; jj < 4; ++jj) b[jj] = sm.B[st][k4 * 4 + gc][wn * BN + grp * 32 + jj * 8 + gr];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         double *row = g.tr + e * (int64_t)g.ncols;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
-          const int col = n0 + j * 8 + 2 * gc;
+          const int col = n0 + wn * BN + j * 8 + 2 * gc;
           if (col + 1 < g.ncols) {
             *reinterpret_cast<double2 *>(row + col) = make_double2(acc[j][i][0], acc[j][i][1]);
           } else if (col < g.ncols) {
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
-          const int r = wm * WM + i * 8 + gr, c = j * 8 + 2 * gc;
+          const int r = wm * WM + i * 8 + gr, c = wn * BN + j * 8 + 2 * gc;
           Cs[r][c] = acc[j][i][0];
           Cs[r][c + 1] = acc[j][i][1];
         }
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         }
       }
       __syncthreads();
-      constexpr int MODES = BN / 3;
+      constexpr int MODES = BNT / 3;   // 32 NH modes, warp column h holds modes [32h, 32h+32)
       constexpr int U = 4;   // items per batch: their 3U loads are in flight together
       const int64_t cs = g.n_tet * g.LD;
       const bool upd = g.out_mode == OUT_UPDATE;
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const int idx = base + u * NTHREADS;
           const int r = idx / MODES, ml = idx - r * MODES;
           const int64_t e = m0 + r;
-          const int b = 32 * nt + ml;
+          const int b = 32 * NH * nt + ml;
           o[u] = (idx < BM * MODES && e < g.n_tet && b < g.N) ? e * g.LD + b : -1;
 #pragma unroll
           for (int cc = 0; cc < 3; ++cc)
@@ -278,7 +283,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const int r = idx / MODES, ml = idx - r * MODES;
           const double *G = Gs[r];
           const double cm = G[6];
-          const double v0 = Cs[r][ml], v1 = Cs[r][32 + ml], v2 = Cs[r][64 + ml];
+          const int hb = (ml >> 5) * BN + (ml & 31);
+          const double v0 = Cs[r][hb], v1 = Cs[r][32 + hb], v2 = Cs[r][64 + hb];
           const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
           const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
           const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
@@ -427,7 +433,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
   g.ktl = D.ktl1[sel];
   g.ktoff = D.ktoff1[sel];
-  g.ntiles_n = D.nc1 / 3 / 32;
+  g.ntiles_n = D.nc1 / 3 / (32 * NH);
   g.n_tet = c->n_tet;
   g.N = c->N;
   g.NF = c->NF;
@@ -459,7 +465,7 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
   g.NC = D.nc2;
   g.ktl = D.ktl2;
   g.ktoff = D.ktoff2;
-  g.ntiles_n = D.nc2 / BN;
+  g.ntiles_n = D.nc2 / BNT;
   g.n_tet = c->n_tet;
   g.N = c->N;
   g.NF = c->NF;

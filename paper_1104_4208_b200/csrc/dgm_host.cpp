@@ -216,12 +216,13 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   static const double T1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
   static const double T2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
   const int N = c->N, NF = c->NF;
-  const int Nk = (N + BK - 1) / BK * BK, NFk = (NF + BK - 1) / BK * BK, Np = (N + 31) / 32 * 32;
+  constexpr int NH = dgm::kDenseNH, BNT = BN * NH;
+  const int Nk = (N + BK - 1) / BK * BK, NFk = (NF + BK - 1) / BK * BK, Np = (N + 32 * NH - 1) / (32 * NH) * (32 * NH);
   const int k1a = 3 * Nk;
   const int K1 = k1a + 8 * NFk;
   const int K2 = 3 * Nk;
   const int nc1 = 3 * Np;
-  const int nc2 = (8 * NF + BN - 1) / BN * BN;
+  const int nc2 = (8 * NF + BNT - 1) / BNT * BNT;
   std::vector<double> B1((size_t)K1 * nc1, 0.0), B2((size_t)K2 * nc2, 0.0);
   // curl: column (c, β) of Ĉ by running the sweep program on that unit input
   int maxslot = 0;
@@ -290,10 +291,11 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     for (int t = 0; t < ntn; ++t) {
       for (int kt = klo / BK; kt < khi / BK; ++kt) {
         uint32_t mask = 0;
-        for (int grp = 0; grp < BN / GW; ++grp)
+        for (int grp = 0; grp < BNT / GW; ++grp)
           for (int cc = 0; cc < GW && !(mask >> grp & 1); ++cc) {
-            const int tc = grp * GW + cc;
-            const int col = gather ? (tc / 32) * Np + 32 * t + tc % 32 : t * BN + tc;
+            const int tc = grp * GW + cc;   // column within the CTA tile; warp column h = tc / 96
+            const int h = tc / BN, t3 = tc % BN;
+            const int col = gather ? (t3 / 32) * Np + 32 * (NH * t + h) + t3 % 32 : t * BNT + tc;
             for (int k = kt * BK; k < (kt + 1) * BK; ++k)
               if (B[(size_t)k * nc + col] != 0.0) {
                 mask |= 1u << grp;
@@ -307,10 +309,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   };
   std::vector<uint32_t> l1[4], l2;
   std::vector<int32_t> o1[4], o2;
-  tiles(B1, nc1, Np / 32, true, 0, k1a, l1[1], o1[1]);
-  tiles(B1, nc1, Np / 32, true, k1a, K1, l1[2], o1[2]);
-  tiles(B1, nc1, Np / 32, true, 0, K1, l1[3], o1[3]);
-  tiles(B2, nc2, nc2 / BN, false, 0, K2, l2, o2);
+  tiles(B1, nc1, Np / (32 * NH), true, 0, k1a, l1[1], o1[1]);
+  tiles(B1, nc1, Np / (32 * NH), true, k1a, K1, l1[2], o1[2]);
+  tiles(B1, nc1, Np / (32 * NH), true, 0, K1, l1[3], o1[3]);
+  tiles(B2, nc2, nc2 / BNT, false, 0, K2, l2, o2);
   if (std::getenv("DGM_DEBUG_DENSE")) {
     auto bits = [](const std::vector<uint32_t> &l) {
       long n = 0;

@@ -80,6 +80,9 @@ struct DevStream {
 // 32).  B2 [3Nk][nc2]: rows c*Nk+β, columns (f*2+k)*NF+γ (trace-buffer order).
 // ktl/ktoff: per n-tile the non-zero k-tiles with a 12-bit mask of non-zero 16x8
 // column groups (sel 1 curl only, 2 flux only, 3 both).
+// warp columns per dense GEMM CTA (CTA tile = 64 elements x 96*kDenseNH columns);
+// the host pads the operator layouts to it
+constexpr int kDenseNH = 1;
 struct DenseOps {
   double *B1 = nullptr, *B2 = nullptr, *AB = nullptr;
   int64_t *koff1 = nullptr, *koff2 = nullptr;
