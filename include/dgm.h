@@ -64,7 +64,7 @@ typedef enum {
 typedef enum {
   DGM_FLUX_CENTRAL = 0,    /* H* = {{H}}, E* = {{E}} */
   DGM_FLUX_UPWIND = 1,     /* Riemann flux, Z = sqrt(μ/ε)               (reading G2)       */
-  DGM_FLUX_STABILIZED = 2  /* central flux + face unknowns H^F with face mass (α/h_F):
+  DGM_FLUX_STABILIZED = 2  /* central flux + face unknowns H^F with face mass (h_F/α):
                               energy-conserving and free of spurious modes
                               (readings G16-G17); use the *_sc calls */
 } dgm_flux;
@@ -161,9 +161,12 @@ dgm_status dgm_energy(dgm_ctx *ctx, const double *E, const double *H, double *ou
  * [[e]] = e⁻ − e⁺ the system (central part per reading G1) is
  *   (εĖ,e)    = central E-eq + Σ_F (H^F×ν_F, [[e]])_F
  *   (μḢ,h)_T  = central H-eq
- *   (α/h_F)(Ḣ^F, h^F)_F = ([[E]]×ν, h^F)_F       (PEC faces: [[E]] = E⁻)
+ *   (h_F/α)(Ḣ^F, h^F)_F = ([[E]]×ν, h^F)_F       (PEC faces: [[E]] = E⁻)
  * with α = alpha0·p², h_F = sqrt(|t₁×t₂|).  It conserves
- * ½(εE,E) + ½(μH,H) + ½Σ_F (α/h_F)(H^F,H^F)_F. */
+ * ½(εE,E) + ½(μH,H) + ½Σ_F (h_F/α)(H^F,H^F)_F.  The face mass h_F/α follows from
+ * H^F := α([[E]]×ν)/(iωh), which makes the added term the
+ * penalty S(E,e) of strength α/h; the printed face equation
+ * has α/h there instead (reading G17). */
 
 /* n_faces and, if face_id != NULL, the face index of every [n_tet][4] slot
  * (host int32).  DGM_EINVAL unless the context is DGM_FLUX_STABILIZED. */
@@ -178,7 +181,7 @@ dgm_status dgm_step_sc(dgm_ctx *ctx, double *E, double *H, double *HF, double dt
 dgm_status dgm_rhs_sc(dgm_ctx *ctx, const double *E, const double *H, const double *HF, double *dE, double *dH,
                       double *dHF, void *cuda_stream);
 
-/* ½(E,MεE) + ½(H,MμH) + ½Σ_F(α/h_F)(H^F,H^F)_F; synchronises. */
+/* ½(E,MεE) + ½(H,MμH) + ½Σ_F(h_F/α)(H^F,H^F)_F; synchronises. */
 dgm_status dgm_energy_sc(dgm_ctx *ctx, const double *E, const double *H, const double *HF, double *out_host,
                          void *cuda_stream);
 

@@ -280,12 +280,18 @@ class TierBStab(TierB):
     the system (signs: reading G1/G16) is
       (εĖ, e)_T      = central E-eq  - Σ_f σ_{T,f} ∫ (H^F_1 e_2 - H^F_2 e_1) du dv
       (μḢ, h)_T      = central H-eq
-      (α/h_F) ∫ Ḣ^F·h^F ds = Σ_{T∋F} σ_{T,f} ∫ (E_2 h_1 - E_1 h_2) du dv
+      (h_F/α) ∫ Ḣ^F·h^F ds = Σ_{T∋F} σ_{T,f} ∫ (E_2 h_1 - E_1 h_2) du dv
     i.e. Σ_F (H^F×ν, [[e]])_F in the E equation and ([[E]]×ν, h^F)_F in the face
     equation with the same sign, which makes the semi-discrete system skew, so
-    ½(εE,E) + ½(μH,H) + ½Σ_F(α/h_F)(H^F,H^F)_F is conserved.
+    ½(εE,E) + ½(μH,H) + ½Σ_F(h_F/α)(H^F,H^F)_F is conserved.
     On a PEC face [[E]] = E⁻ (one side).  Readings: α = alpha0·p²,
-    h_F = sqrt(|t₁×t₂|) (G16).  Per face mode γ the face mass is (α/h_F) M ‖ψ_γ‖²
+    h_F = sqrt(|t₁×t₂|) (G16).  Face mass h_F/α (reading G17): it follows from the
+    definition H^F := α([[E]]×ν)/(iωh), i.e. iωH^F = (α/h)[[E]]×ν,
+    which is what makes the added term the penalty S(E,e) = Σ(α/h)([[E]]×ν,[[e]]×ν)
+     of the second-order form; the printed face equation
+     puts α/h on the other side, which would make the penalty
+    h/α and weaken it as α ~ p² grows.  Pinned by the cavity resonances
+    (tests/test_oracle_stab.py).  Per face mode γ the face mass is (h_F/α) M ‖ψ_γ‖²
     with M = |t₁×t₂| g⁻¹ (as for the upwind flux)."""
 
     def __init__(self, xyz, tet, rep, p, eps, mu, alpha0=1.0):
@@ -327,7 +333,7 @@ class TierBStab(TierB):
         return out
 
     def dHF(self, E):
-        """Ḣ^F_γ = (h_F/α) M⁻¹ Σ_{T∋F} σ_{T,f} (E_2, -E_1)_γ."""
+        """Ḣ^F_γ = (α/h_F) M⁻¹ Σ_{T∋F} σ_{T,f} (E_2, -E_1)_γ (reading G17)."""
         trE = self.traces(E)                                                   # [n,4,2,NF]
         NF = trE.shape[-1]
         rhs = np.zeros((self.n_faces, 2, NF))
@@ -338,14 +344,14 @@ class TierBStab(TierB):
                 rhs[k, 0] += s * trE[T, f, 1]
                 rhs[k, 1] -= s * trE[T, f, 0]
         Minv = np.linalg.inv(self.Mf)
-        return (self.hF / self.alpha)[:, None, None] * np.einsum("fkl,flg->fkg", Minv, rhs)
+        return (self.alpha / self.hF)[:, None, None] * np.einsum("fkl,flg->fkg", Minv, rhs)
 
     def energy(self, E, H, HF=None):
         w = super().energy(E, H)
         if HF is not None:
             fn = self.R["fnorms"]
             q = np.einsum("fkg,fkl,flg->fg", HF, self.Mf, HF) @ fn
-            w += 0.5 * float(np.sum(self.alpha / self.hF * q))
+            w += 0.5 * float(np.sum(self.hF / self.alpha * q))
         return w
 
 

@@ -576,7 +576,7 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
       G[0] = g11 / area;   // M^{-1} = g / |t1×t2|
       G[1] = g12 / area;
       G[2] = g22 / area;
-      G[3] = std::sqrt(area) / c->alpha;   // h_F / α, h_F = sqrt(|t1×t2|) (reading G16)
+      G[3] = c->alpha / std::sqrt(area);   // α / h_F: Ḣ^F factor (reading G17), h_F = sqrt(|t1×t2|) (G16)
       G[4] = g22 / area;   // M = |t1×t2| g^{-1}
       G[5] = -g12 / area;
       G[6] = g11 / area;

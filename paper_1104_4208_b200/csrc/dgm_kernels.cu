@@ -587,7 +587,7 @@ __global__ void seed_kernel(double *X, uint64_t seed, int64_t n_tet, int N, int 
 }
 
 // Stabilised central flux, face equation (signs reading G16):
-//   Ḣ^F_γ = (h_F/α) M^{-1} Σ_{T∋F} σ_{T,f} (E_2, -E_1)_{T,f,γ}
+//   Ḣ^F_γ = (α/h_F) M^{-1} Σ_{T∋F} σ_{T,f} (E_2, -E_1)_{T,f,γ}   (face mass h_F/α, reading G17)
 // from the tangential traces of E in the trace buffer (both layouts); one thread per
 // (face, mode).  HF += dt Ḣ^F (update) or dHF = Ḣ^F (write).
 __global__ void hf_kernel(const double *__restrict__ TE, double *HF, double *dHF, double dt,
@@ -630,7 +630,7 @@ __global__ void hf_kernel(const double *__restrict__ TE, double *HF, double *dHF
   }
 }
 
-// ½ Σ_F (α/h_F) Σ_γ ‖ψ_γ‖² H_γᵀ M H_γ  (face part of the stabilised energy)
+// ½ Σ_F (h_F/α) Σ_γ ‖ψ_γ‖² H_γᵀ M H_γ  (face part of the stabilised energy; fgeo[3] = α/h_F)
 __global__ void face_energy_kernel(const double *__restrict__ HF, const double *__restrict__ fgeo,
                                    const double *__restrict__ fnorms, int64_t n_faces, int NF, double *partial) {
   double sum = 0.0;
