@@ -364,3 +364,39 @@ def symplectic_euler_stab(B, E, H, HF, dt, nsteps):
         H, HF = H + dt * dH, HF + dt * dHF
         E = E + dt * B.dE(E, H, HF)
     return E, H, HF
+
+
+class TierBMixed:
+    """Mixed orders E ∈ P^q, H ∈ P^{q-1} (the paper's spaces; NEXT-2).
+
+    The Dubiner basis is hierarchical in graded order, so P^{q-1} is the first
+    N(q-1) modes of P^q and the reference mass is diagonal in the modes.  Hence,
+    for the central and upwind fluxes, the mixed scheme is the order-q scheme with
+    H embedded (modes >= N(q-1) zero) and the H equation tested only against
+    P^{q-1}, i.e. truncated to its first N(q-1) modes:
+      Ė = Ė_q(E, H),   Ḣ = trunc(Ḣ_q(E, H)),
+    where the E equation's test space is all of P^q (the embedded H is represented
+    exactly) and the H equation's rows for modes < N(q-1) are exactly the mixed
+    scheme's (same integrals, same diagonal mass).  Fields use the order-q layout;
+    H's modes >= N(q-1) are ignored on input and returned as zero."""
+
+    def __init__(self, xyz, tet, rep, q, eps, mu, flux="central"):
+        assert q >= 2 and flux in ("central", "upwind")
+        self.B = TierB(xyz, tet, rep, q, eps, mu, flux)
+        self.q, self.N = q, self.B.N
+        self.NH = q * (q + 1) * (q + 2) // 6   # N(q-1)
+        self.n_tet = self.B.n_tet
+
+    def _h(self, H):
+        Hm = np.array(H, dtype=np.float64, copy=True)
+        Hm[..., self.NH:] = 0.0
+        return Hm
+
+    def dE(self, E, H, part="all"):
+        return self.B.dE(E, self._h(H), part)
+
+    def dH(self, E, H, part="all"):
+        return self._h(self.B.dH(E, self._h(H), part))
+
+    def energy(self, E, H):
+        return self.B.energy(E, self._h(H))
