@@ -96,6 +96,12 @@ typedef struct {
   int32_t mu_per_elem;   /* same for mu                                       */
   double alpha0;         /* DGM_FLUX_STABILIZED: α = alpha0·p² (≤0 → 1)       */
   int32_t engine;        /* dgm_engine_kind                                   */
+  int32_t mixed_order;   /* 0: E and H of degree `order`.  1: the paper's spaces
+                            E ∈ P^order, H ∈ P^(order-1); needs
+                            order >= 2, central or upwind flux, and the dense engine
+                            (AUTO resolves to it).  Both fields keep the order-`order`
+                            layout; H's modes >= N(order-1) are ignored by the
+                            operator and stay zero when zero on input.            */
 } dgm_opts;
 
 /* Validate the mesh, match faces, compute per-element geometry

@@ -37,7 +37,7 @@ class _Mesh(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32),
-                ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32)]
+                ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32), ("mixed_order", ctypes.c_int32)]
 
 
 _lib = None
@@ -110,7 +110,8 @@ def dgm_match_faces_host(xyz, tet, rep=None):
 class Context:
     """Owns a dgm_ctx.  Methods mirror the C ABI names (dgm_*)."""
 
-    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0, engine="auto"):
+    def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0, engine="auto",
+                 mixed_order=False):
         lib = load_library()
         self._lib = lib
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
@@ -121,7 +122,10 @@ class Context:
         self._keep = (xyz, tet, repa, eps_a, mu_a)
         m = _Mesh(xyz.shape[0], xyz.ctypes.data, tet.shape[0], tet.ctypes.data,
                   None if repa is None else repa.ctypes.data)
-        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0), ENGINE[engine])
+        o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0), ENGINE[engine],
+                  int(bool(mixed_order)))
+        # H's live modes: N(p-1) for mixed orders (E ∈ P^p, H ∈ P^{p-1}), else N
+        self.NH = p * (p + 1) * (p + 2) // 6 if mixed_order else (p + 1) * (p + 2) * (p + 3) // 6
         h = ctypes.c_void_p()
         st = lib.dgm_create(ctypes.byref(m), int(p), eps_a.ctypes.data, mu_a.ctypes.data, ctypes.byref(o), ctypes.byref(h))
         if st != DGM_OK:

@@ -405,6 +405,7 @@ dgm_status gemm_go(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
 
 dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
   const DenseOps &D = c->dense;
+  const int v = a.stage == STAGE_E ? 0 : 1;   // updated field: operator variant (mixed orders)
   if (a.do_flux) {
     const int64_t total = a.n_tet * 4 * c->NF;
     int64_t grid = (total + 255) / 256;
@@ -426,13 +427,13 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.k1 = D.k1a;
   g.Nk = D.k1a / 3;
   g.NFk = (c->NF + BK - 1) / BK * BK;
-  g.Bm = D.B1;
+  g.Bm = D.B1[v];
   g.NC = D.nc1;
   g.Np = D.nc1 / 3;
   // curl only / flux only: restrict the k-tile lists
   const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
-  g.ktl = D.ktl1[sel];
-  g.ktoff = D.ktoff1[sel];
+  g.ktl = D.ktl1[v][sel];
+  g.ktoff = D.ktoff1[v][sel];
   g.ntiles_n = D.nc1 / 3 / (32 * NH);
   g.n_tet = c->n_tet;
   g.N = c->N;
@@ -447,11 +448,11 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.out_mode = a.out_mode;
   dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
   if (s != DGM_OK) return s;
-  if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st);
+  if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st, v);
   return DGM_OK;
 }
 
-dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
+dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field) {
   const DenseOps &D = c->dense;
   GemmArgs g{};
   g.p0 = X;
@@ -461,10 +462,10 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
   g.k1 = 1 << 30;
   g.Nk = D.k1a / 3;
   g.NFk = (c->NF + BK - 1) / BK * BK;
-  g.Bm = D.B2;
+  g.Bm = D.B2[field];
   g.NC = D.nc2;
-  g.ktl = D.ktl2;
-  g.ktoff = D.ktoff2;
+  g.ktl = D.ktl2[field];
+  g.ktoff = D.ktoff2[field];
   g.ntiles_n = D.nc2 / BNT;
   g.n_tet = c->n_tet;
   g.N = c->N;

@@ -274,13 +274,6 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   };
   clean(B1);
   clean(B2);
-  // A-operand column offsets (element stride applied in the kernel); -1 = zero row
-  const int64_t cs = c->n_tet * c->LD;
-  std::vector<int64_t> ko1(K1, -1), ko2(K2, -1);
-  for (int cc = 0; cc < 3; ++cc)
-    for (int b = 0; b < N; ++b) ko1[cc * Nk + b] = ko2[cc * Nk + b] = (int64_t)cc * cs + b;
-  for (int jj = 0; jj < 8; ++jj)
-    for (int g = 0; g < NF; ++g) ko1[k1a + jj * NFk + g] = (int64_t)jj * NF + g;
   // per n-tile: non-zero k-tiles with the mask of non-zero 16x32 column blocks
   // (one per warp column of the GEMM CTA)
   constexpr int GW = 32;
@@ -307,50 +300,83 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
       ktoff.push_back((int32_t)ktl.size());
     }
   };
-  std::vector<uint32_t> l1[4], l2;
-  std::vector<int32_t> o1[4], o2;
-  tiles(B1, nc1, Np / (32 * NH), true, 0, k1a, l1[1], o1[1]);
-  tiles(B1, nc1, Np / (32 * NH), true, k1a, K1, l1[2], o1[2]);
-  tiles(B1, nc1, Np / (32 * NH), true, 0, K1, l1[3], o1[3]);
-  tiles(B2, nc2, nc2 / BNT, false, 0, K2, l2, o2);
+  // variants per updated field (0: E, 1: H); mixed orders (H ∈ P^{p-1}, NH = N(p-1)):
+  // the E stage ignores H's modes >= NH as curl input, the H stage has no outputs
+  // there, and H's traces ignore them (face modes > p of the lift/trace vanish exactly
+  // for volume modes of degree <= p-1, so nothing else changes)
+  std::vector<double> B1v[2], B2v[2];
+  const int nvar = c->mixed ? 2 : 1;
+  B1v[0] = B1;
+  B2v[0] = B2;
+  if (c->mixed) {
+    const int NHm = c->NH;
+    B1v[1] = B1;
+    B2v[1] = B2;
+    for (int cc = 0; cc < 3; ++cc)
+      for (int b = NHm; b < N; ++b) {
+        std::fill_n(&B1v[0][(size_t)(cc * Nk + b) * nc1], nc1, 0.0);   // H as curl input
+        std::fill_n(&B2v[1][(size_t)(cc * Nk + b) * nc2], nc2, 0.0);   // H traces
+      }
+    for (size_t k = 0; k < (size_t)K1; ++k)
+      for (int m = 0; m < 3; ++m)
+        for (int b = NHm; b < Np; ++b) B1v[1][k * nc1 + (size_t)m * Np + b] = 0.0;   // H outputs
+  }
+  std::vector<uint32_t> l1[2][4], l2[2];
+  std::vector<int32_t> o1[2][4], o2[2];
+  for (int v = 0; v < nvar; ++v) {
+    tiles(B1v[v], nc1, Np / (32 * NH), true, 0, k1a, l1[v][1], o1[v][1]);
+    tiles(B1v[v], nc1, Np / (32 * NH), true, k1a, K1, l1[v][2], o1[v][2]);
+    tiles(B1v[v], nc1, Np / (32 * NH), true, 0, K1, l1[v][3], o1[v][3]);
+    tiles(B2v[v], nc2, nc2 / BNT, false, 0, K2, l2[v], o2[v]);
+  }
   if (std::getenv("DGM_DEBUG_DENSE")) {
     auto bits = [](const std::vector<uint32_t> &l) {
       long n = 0;
-      for (uint32_t v : l) n += __builtin_popcount(v >> 16);
+      for (uint32_t x : l) n += __builtin_popcount(x >> 16);
       return n;
     };
     std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x32)\n", c->p,
-                 l1[3].size(), bits(l1[3]), l2.size(), bits(l2));
+                 l1[0][3].size(), bits(l1[0][3]), l2[0].size(), bits(l2[0]));
   }
   // one device allocation
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  size_t bytes = al(B1.size() * 8) + al(B2.size() * 8) + al((size_t)K1 * 8) + al((size_t)K2 * 8) +
-                 al(l2.size() * 4 + 4) + al(o2.size() * 4);
-  for (int i = 1; i < 4; ++i) bytes += al(l1[i].size() * 4 + 4) + al(o1[i].size() * 4);
+  size_t bytes = 0;
+  for (int v = 0; v < nvar; ++v) {
+    bytes += al(B1.size() * 8) + al(B2.size() * 8) + al(l2[v].size() * 4 + 4) + al(o2[v].size() * 4);
+    for (int i = 1; i < 4; ++i) bytes += al(l1[v][i].size() * 4 + 4) + al(o1[v][i].size() * 4);
+  }
   CUDA_TRY(c, cudaMalloc(&c->d_dense, bytes));
   char *base = (char *)c->d_dense;
   size_t off = 0;
+  bool ok = true;
   auto put = [&](const void *src, size_t b) -> char * {
     char *d = base + off;
-    if (b) {
-      cudaError_t e = cudaMemcpy(d, src, b, cudaMemcpyHostToDevice);
-      if (e != cudaSuccess) return nullptr;
-    }
-    off += al(b + (b == 0 ? 2 : 0));
+    if (b && cudaMemcpy(d, src, b, cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+    off += al(b + (b == 0 ? 4 : 0));
     return d;
   };
   dgm::DenseOps &D = c->dense;
-  D.B1 = (double *)put(B1.data(), B1.size() * 8);
-  D.B2 = (double *)put(B2.data(), B2.size() * 8);
-  D.koff1 = (int64_t *)put(ko1.data(), ko1.size() * 8);
-  D.koff2 = (int64_t *)put(ko2.data(), ko2.size() * 8);
-  for (int i = 1; i < 4; ++i) {
-    D.ktl1[i] = (uint32_t *)put(l1[i].data(), l1[i].size() * 4);
-    D.ktoff1[i] = (int32_t *)put(o1[i].data(), o1[i].size() * 4);
+  for (int v = 0; v < nvar; ++v) {
+    D.B1[v] = (double *)put(B1v[v].data(), B1v[v].size() * 8);
+    D.B2[v] = (double *)put(B2v[v].data(), B2v[v].size() * 8);
+    for (int i = 1; i < 4; ++i) {
+      D.ktl1[v][i] = (uint32_t *)put(l1[v][i].data(), l1[v][i].size() * 4);
+      D.ktoff1[v][i] = (int32_t *)put(o1[v][i].data(), o1[v][i].size() * 4);
+    }
+    D.ktl2[v] = (uint32_t *)put(l2[v].data(), l2[v].size() * 4);
+    D.ktoff2[v] = (int32_t *)put(o2[v].data(), o2[v].size() * 4);
   }
-  D.ktl2 = (uint32_t *)put(l2.data(), l2.size() * 4);
-  D.ktoff2 = (int32_t *)put(o2.data(), o2.size() * 4);
-  if (!D.B1 || !D.B2 || !D.ktoff2) return dgm::set_err(c, DGM_ECUDA, "dense_build: upload failed");
+  if (!ok) return dgm::set_err(c, DGM_ECUDA, "dense_build: upload failed");
+  if (nvar == 1) {   // equal orders: both fields use the same operators
+    D.B1[1] = D.B1[0];
+    D.B2[1] = D.B2[0];
+    for (int i = 1; i < 4; ++i) {
+      D.ktl1[1][i] = D.ktl1[0][i];
+      D.ktoff1[1][i] = D.ktoff1[0][i];
+    }
+    D.ktl2[1] = D.ktl2[0];
+    D.ktoff2[1] = D.ktoff2[0];
+  }
   D.nc1 = nc1;
   D.nc2 = nc2;
   D.k1a = k1a;
@@ -391,7 +417,7 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   if (order < 1 || order > DGM_PMAX)
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
-  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO};
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0};
   if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_DENSE) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
   if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
     return dgm::set_err(c, DGM_EINVAL, "unknown flux");
@@ -407,6 +433,15 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   c->engine = o.engine == DGM_ENGINE_DENSE ? 1 : o.engine == DGM_ENGINE_SPARSE ? 0 : (p >= 6 ? 1 : 0);
   if (o.engine == DGM_ENGINE_AUTO)
     if (const char *v = std::getenv("DGM_ENGINE")) c->engine = std::strcmp(v, "dense") == 0 ? 1 : 0;
+  // mixed orders E ∈ P^p, H ∈ P^{p-1}: dense engine, central/upwind
+  if (o.mixed_order) {
+    if (p < 2) return dgm::set_err(c, DGM_EORDER, "mixed orders need order >= 2");
+    if (o.flux == DGM_FLUX_STABILIZED) return dgm::set_err(c, DGM_EINVAL, "mixed orders: central or upwind flux only");
+    if (o.engine == DGM_ENGINE_SPARSE) return dgm::set_err(c, DGM_EINVAL, "mixed orders need the dense engine");
+    c->engine = 1;
+    c->mixed = 1;
+  }
+  c->NH = c->mixed ? p * (p + 1) * (p + 2) / 6 : c->N;
   auto rep = [&](int32_t v) -> int64_t { return m->rep ? (int64_t)m->rep[v] : (int64_t)v; };
 
   // ---- validate vertex ids and canonical (ascending-rep) order
@@ -733,8 +768,8 @@ dgm_status dgm_apply_flux(dgm_ctx *c, const double *E, const double *H, double *
   // (and, upwind, E's own), the H equation the other way round
   double *TE = c->d_tr[0], *TH = c->d_tr[2];
   c->tr_valid = false;   // the buffers now hold the traces of these E, H
-  dgm_status s = dgm::launch_tb_traces(c, E, TE, st);
-  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st);
+  dgm_status s = dgm::launch_tb_traces(c, E, TE, st, 0);
+  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st, 1);
   if (s == DGM_OK && dE) s = dgm::launch_tb_stage(c, dgm::STAGE_E, H, nullptr, dE, 0.0, 0, 1, om, TH, TE, nullptr, st);
   if (s == DGM_OK && dH) s = dgm::launch_tb_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 0, 1, om, TE, TH, nullptr, st);
   return s;
@@ -760,9 +795,9 @@ dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps
     ch = c->tr_ch;
     if (before_h) cudaStreamWaitEvent(st, before_h, 0);
   } else {
-    r = dgm::launch_tb_traces(c, E, c->d_tr[0], st);
+    r = dgm::launch_tb_traces(c, E, c->d_tr[0], st, 0);
     if (before_h) cudaStreamWaitEvent(st, before_h, 0);   // H has arrived
-    if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st);
+    if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st, 1);
   }
   c->tr_valid = false;
   for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
@@ -862,8 +897,8 @@ dgm_status dgm_rhs_sc(dgm_ctx *c, const double *E, const double *H, const double
   c->launches = 0;
   c->tr_valid = false;
   double *TE = c->d_tr[0], *TH = c->d_tr[2];
-  dgm_status s = dgm::launch_tb_traces(c, E, TE, st);
-  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st);
+  dgm_status s = dgm::launch_tb_traces(c, E, TE, st, 0);
+  if (s == DGM_OK) s = dgm::launch_tb_traces(c, H, TH, st, 1);
   if (s == DGM_OK && dH) s = dgm::launch_tb_stage(c, dgm::STAGE_H, E, nullptr, dH, 0.0, 1, 1, dgm::OUT_WRITE, TE, TH, nullptr, st);
   if (s == DGM_OK && dHF) s = dgm::launch_hf(c, TE, nullptr, dHF, 0.0, st);
   if (s == DGM_OK && dE) {
@@ -906,14 +941,14 @@ dgm_status dgm_spectral_radius(dgm_ctx *c, int iters, uint64_t seed, double *rho
     if ((r = dgm::launch_scale(c, Hv, Hv, 1.0 / std::sqrt(nrm2), st)) != DGM_OK) break;
     // D = Ė(0, H) = -Mε^{-1} Cᵀ H   (curl + face parts; upwind E-terms vanish for E = 0)
     CUDA_TRY(c, cudaMemsetAsync(Z, 0, bytes, st));
-    if ((r = dgm::launch_tb_traces(c, Hv, c->d_tr[2], st)) != DGM_OK) break;
-    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[0], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, Hv, c->d_tr[2], st, 1)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[0], st, 0)) != DGM_OK) break;
     if ((r = dgm::launch_tb_stage(c, dgm::STAGE_E, Hv, nullptr, D, 0.0, 1, 1, dgm::OUT_WRITE, c->d_tr[2], c->d_tr[0],
                                   nullptr, st)) != DGM_OK)
       break;
     // W = Ḣ(D, 0) = Mμ^{-1} C D
-    if ((r = dgm::launch_tb_traces(c, D, c->d_tr[0], st)) != DGM_OK) break;
-    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[2], st)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, D, c->d_tr[0], st, 0)) != DGM_OK) break;
+    if ((r = dgm::launch_tb_traces(c, Z, c->d_tr[2], st, 1)) != DGM_OK) break;
     if ((r = dgm::launch_tb_stage(c, dgm::STAGE_H, D, nullptr, W, 0.0, 1, 1, dgm::OUT_WRITE, c->d_tr[0], c->d_tr[2],
                                   nullptr, st)) != DGM_OK)
       break;

@@ -83,14 +83,16 @@ struct DevStream {
 // warp columns per dense GEMM CTA (CTA tile = 64 elements x 96*kDenseNH columns);
 // the host pads the operator layouts to it
 constexpr int kDenseNH = 1;
+// Per updated field v (0: E stage / E traces, 1: H stage / H traces) a variant of the
+// matrices; they differ only for mixed orders (H ∈ P^{p-1}: B1[0] ignores H's modes
+// >= N(p-1) as curl input, B1[1] has no output columns there, B2[1] no rows there).
 struct DenseOps {
-  double *B1 = nullptr, *B2 = nullptr, *AB = nullptr;
-  int64_t *koff1 = nullptr, *koff2 = nullptr;
+  double *B1[2] = {nullptr, nullptr}, *B2[2] = {nullptr, nullptr}, *AB = nullptr;
   int nc1 = 0, nc2 = 0, k1a = 0;
-  uint32_t *ktl1[4] = {nullptr, nullptr, nullptr, nullptr};
-  int32_t *ktoff1[4] = {nullptr, nullptr, nullptr, nullptr};
-  uint32_t *ktl2 = nullptr;
-  int32_t *ktoff2 = nullptr;
+  uint32_t *ktl1[2][4] = {};
+  int32_t *ktoff1[2][4] = {};
+  uint32_t *ktl2[2] = {nullptr, nullptr};
+  int32_t *ktoff2[2] = {nullptr, nullptr};
 };
 
 struct DevProgs {
@@ -137,6 +139,8 @@ struct dgm_ctx {
   int sms = 0;
   int ho_stream = 1;   // sparse, p > kLanePmax: streamed-table kernels (DGM_HO_STREAM=0: one-element CTA kernels)
   int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
+  int mixed = 0;       // 1: H ∈ P^{p-1} (E ∈ P^p), dense engine only; NH = N(p-1)
+  int NH = 0;
   dgm::DenseOps dense{};
   void *d_dense = nullptr;
   dgm::DevStream stream{};
@@ -183,7 +187,7 @@ dgm_status set_err(dgm_ctx *c, dgm_status s, const std::string &msg);
 dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, double *dX, double dt, int do_curl,
                            int do_flux, int out_mode, const double *trY, const double *trX, double *trOut,
                            cudaStream_t st);
-dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
+dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field);   // field: 0 E, 1 H
 dgm_status launch_energy(dgm_ctx *c, const double *E, const double *H, double *out_host, cudaStream_t st);
 dgm_status launch_hf(dgm_ctx *c, const double *TE, double *HF, double *dHF, double dt, cudaStream_t st);
 dgm_status launch_face_energy(dgm_ctx *c, const double *HF, double *out, cudaStream_t st);
@@ -192,7 +196,7 @@ dgm_status launch_scale(dgm_ctx *c, double *X, const double *Y, double s, cudaSt
 dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
 // dense-contraction engine (dgm_dense.cu), all orders
 dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
-dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st);
+dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field);
 // trace buffers use the 16-element interleaved layout only on the sparse lane path
 inline bool lane_layout(const dgm_ctx *c);
 

@@ -518,9 +518,9 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
   DGM_DISPATCH_HI(c->p, launch_stage2_p, c, a, trY, trOut, st)
 }
 
-dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
+dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field) {
   if (c->n_tet == 0) return DGM_OK;
-  if (c->engine == 1) return launch_dense_traces(c, X, tr, st);
+  if (c->engine == 1) return launch_dense_traces(c, X, tr, st, field);
   if (c->p <= kLanePmax) return launch_lane_traces(c, X, tr, st);
   if (c->ho_stream) return launch_stream_traces(c, X, tr, st);
   DGM_DISPATCH_HI(c->p, launch_trace2_p, c, X, tr, st)
