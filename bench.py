@@ -212,13 +212,14 @@ def run_ours(args, rank, world):
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            tr = json.load(f).get(args.config)
-        if tr and tr.get("kernel") == kern:
-            traffic = tr["dram_bytes_per_launch"]
+            tj = json.load(f)
+        for tr in (tj.get(args.config), tj.get(args.config + "_dense")):
+            if tr and tr.get("kernel") == kern:
+                traffic = tr["dram_bytes_per_launch"]
     res["engine"] = engine
     res["roofline"] = {"bound": "hbm", "achieved": B / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
                        "frac": (B / per_launch_s / 1e9) / hbm, "traffic": traffic,
-                       "traffic_source": "profiles/r01_traffic.json (one ncu --set full capture, bytes per launch)"
+                       "traffic_source": "profiles/r01_traffic.json (ncu dram__bytes_read+write per launch; dense: per stage)"
                        if traffic is not None else None,
                        "kernel": kern, "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
                        "launches_per_step": launches / args.steps,

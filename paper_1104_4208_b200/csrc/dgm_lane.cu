@@ -16,6 +16,7 @@
 // trace stores of a half-warp are single 128-byte transactions.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "dgm_internal.h"
 #include "lane/lane_p1.cuh"
@@ -396,6 +397,10 @@ static int occupancy_grid(dgm_ctx *c, K kernel, int warps, size_t smem, int64_t 
 // sequence of 16-element groups, so the last round can be nearly empty.  Pick w
 // minimising rounds(w) * w^0.55 (per-SM throughput measured to grow ~ w^0.45).
 static int pick_warps(int64_t n_tet, int sms, int wmax, int ctas_per_sm_for_w1) {
+  if (const char *v = std::getenv("DGM_LANE_WARPS")) {   // experiments only
+    const int w = std::atoi(v);
+    if (w >= 1 && w <= wmax) return w;
+  }
   const int64_t groups = (n_tet + 15) / 16;
   double best = 1e300;
   int bw = wmax;
