@@ -280,3 +280,32 @@ def test_spectral_radius_vs_dense_eigen():
     Ed, Hd = c.to_device(E), c.to_device(H)
     c.dgm_step(Ed, Hd, 1.2 * dtmax, 400)
     assert not (c.dgm_energy(Ed, Hd) < 1e6 * w0)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("flux", ["central", "upwind"])
+def test_single_tet_degenerate_mesh(engine, flux):
+    """Degenerate case: one tetrahedron, all four faces PEC (every element tile and
+    16-element group is ragged).  Apply and 20 steps against tier B; a zero-step call
+    is a no-op."""
+    p = 5
+    xyz = np.array([[0.1, 0.0, 0.0], [1.0, 0.1, 0.0], [0.0, 0.9, 0.2], [0.1, 0.2, 1.1]])
+    tet = np.array([[0, 1, 2, 3]], dtype=np.int32)
+    from paper_1104_4208_b200 import Context
+    c = Context(xyz, tet, p, eps=2.0, mu=1.5, flux=flux, engine=engine)
+    B = TierB(xyz, tet, None, p, 2.0, 1.5, flux)
+    rng = np.random.default_rng(1)
+    E = rng.standard_normal((3, 1, c.N))
+    H = rng.standard_normal((3, 1, c.N))
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    dE, dH = c.empty_field(), c.empty_field()
+    c.dgm_apply_curl(Ed, Hd, dE, dH)
+    c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
+    assert rel_err(c.to_host(dE), B.dE(E, H)) <= TOL_APPLY
+    assert rel_err(c.to_host(dH), B.dH(E, H)) <= TOL_APPLY
+    c.dgm_step(Ed, Hd, 1e-3, 0)
+    assert np.array_equal(c.to_host(Ed), E)
+    c.dgm_step(Ed, Hd, 1e-3, 20)
+    Er, Hr, _ = symplectic_euler(B, E, H, 1e-3, 20)
+    assert rel_err(c.to_host(Ed), Er) <= TOL_STEPS
+    assert rel_err(c.to_host(Hd), Hr) <= TOL_STEPS

@@ -70,3 +70,15 @@ def test_mesh_errors(lib):
     dup = np.concatenate([m.tet, m.tet[:1], m.tet[:1]])
     with pytest.raises(DgmError):
         dgm_match_faces_host(m.xyz, dup)
+
+
+def test_empty_and_out_of_range_meshes_rejected(lib):
+    """Empty input and bad vertex ids fail with an error code, not a crash."""
+    from paper_1104_4208_b200.binding import dgm_match_faces_host, DgmError
+    m = di.kuhn_mesh(2)
+    with pytest.raises(DgmError):
+        dgm_match_faces_host(m.xyz, np.zeros((0, 4), dtype=np.int32))
+    bad = m.tet.copy()
+    bad[3, 3] = m.xyz.shape[0] + 5
+    with pytest.raises(DgmError):
+        dgm_match_faces_host(m.xyz, bad)
