@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -37,7 +38,9 @@ METRIC = "DOF-updates/s per DG time step (FP64) and % of HBM/FP64 roofline, 1 B2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: enough for ~0.25 s of GPU time, so the clock sampler "
+                         "sees the timed region; 3 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=list(di.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -161,6 +164,16 @@ def run_ours(args, rank, world):
     for _ in range(max(0, args.warmup - 1)):
         ctx.dgm_step_ex(Ed, Hd, dt, 1, DGM_STEP_CONTINUE)
     torch.cuda.synchronize()
+    if args.steps is None:
+        # size the timed region to ~0.25 s of GPU time (same K on every rank)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            ctx.dgm_step_ex(Ed, Hd, dt, 1, DGM_STEP_CONTINUE)
+        e1.record(stream)
+        e1.synchronize()
+        t_step = max(e0.elapsed_time(e1) / 3e3, 1e-6)
+        args.steps = int(dist_max(float(min(4000, max(5, math.ceil(0.25 / t_step)))), world))
     dist_barrier(world)
     launches = 0
     times = []
@@ -303,6 +316,8 @@ def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference" and args.steps is None:
+        args.steps = 3
     if args.impl == "reference":
         if rank != 0:
             return 0
