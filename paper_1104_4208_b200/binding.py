@@ -149,6 +149,18 @@ class Context:
             raise ValueError(f"{name} must be a contiguous CUDA float64 tensor of shape (3, {self.n_tet}, {self.ld})")
         return t
 
+    def _faces(self, t, name):
+        import torch
+        if t is None:
+            return None
+        if not hasattr(self, "_nfaces"):
+            self._nfaces = self.dgm_faces()[0]
+        NF = (self.p + 1) * (self.p + 2) // 2
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                and tuple(t.shape) == (self._nfaces, 2, NF)):
+            raise ValueError(f"{name} must be a contiguous CUDA float64 tensor of shape ({self._nfaces}, 2, {NF})")
+        return t
+
     def empty_field(self):
         import torch
         return torch.zeros((3, self.n_tet, self.ld), dtype=torch.float64, device="cuda")
@@ -211,17 +223,21 @@ class Context:
         return torch.zeros((nf, 2, NF), dtype=torch.float64, device="cuda")
 
     def dgm_step_sc(self, E, H, HF, dt, nsteps=1, flags=0, stream=None):
-        self._check(self._lib.dgm_step_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
+        self._check(self._lib.dgm_step_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
+                                          _ptr(self._faces(HF, "HF")),
                                           float(dt), int(nsteps), int(flags), _stream(stream)))
 
     def dgm_rhs_sc(self, E, H, HF, dE=None, dH=None, dHF=None, stream=None):
-        self._check(self._lib.dgm_rhs_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
-                                         _ptr(self._field(dE, "dE")), _ptr(self._field(dH, "dH")), _ptr(dHF),
+        self._check(self._lib.dgm_rhs_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
+                                         _ptr(self._faces(HF, "HF")),
+                                         _ptr(self._field(dE, "dE")), _ptr(self._field(dH, "dH")),
+                                         _ptr(self._faces(dHF, "dHF")),
                                          _stream(stream)))
 
     def dgm_energy_sc(self, E, H, HF, stream=None):
         out = ctypes.c_double()
-        self._check(self._lib.dgm_energy_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")), _ptr(HF),
+        self._check(self._lib.dgm_energy_sc(self.h, _ptr(self._field(E, "E")), _ptr(self._field(H, "H")),
+                                            _ptr(self._faces(HF, "HF")),
                                             ctypes.byref(out), _stream(stream)))
         return out.value
 
