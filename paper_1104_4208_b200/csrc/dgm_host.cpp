@@ -386,6 +386,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
 
 void free_ctx(dgm_ctx *c) {
   if (!c) return;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
+  for (int i = 0; i < 2; ++i)
+    if (c->gev[i]) cudaEventDestroy(c->gev[i]);
   cudaFree(c->d_dense);
   cudaFree(c->dense.AB);
   cudaFree(c->d_stream);
@@ -630,6 +634,7 @@ dgm_status upload_impl(dgm_ctx *c) {
   CUDA_TRY(c, cudaGetDevice(&dev));
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
   if (const char *v = std::getenv("DGM_HO_STREAM")) c->ho_stream = std::atoi(v) != 0;
+  if (const char *v = std::getenv("DGM_GRAPHS")) c->use_graphs = std::atoi(v) != 0;
   CUDA_TRY(c, cudaMalloc(&c->d_geo, sizeof(Geo) * n));
   CUDA_TRY(c, cudaMemcpy(c->d_geo, c->h_geo.data(), sizeof(Geo) * n, cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMalloc(&c->d_nbr, 4 * sizeof(int32_t) * n));
@@ -800,20 +805,69 @@ dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps
     if (r == DGM_OK && up) r = dgm::launch_tb_traces(c, H, c->d_tr[2], st, 1);
   }
   c->tr_valid = false;
-  for (int64_t s = 0; s < nsteps && r == DGM_OK; ++s) {
+  // one symplectic-Euler step on stream ss (ce, ch: current trace-buffer parities)
+  auto one_step = [&](cudaStream_t ss, bool last) -> dgm_status {
     double *TE = c->d_tr[ce], *THr = c->d_tr[2 + ch], *THw = c->d_tr[2 + (up ? 1 - ch : ch)];
-    r = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, st);
+    dgm_status q = dgm::launch_tb_stage(c, dgm::STAGE_H, E, H, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TE, THr, THw, ss);
     if (up) ch = 1 - ch;
-    if (r != DGM_OK) break;
+    if (q != DGM_OK) return q;
     // stabilised flux: H^F += dt Ḣ^F(E^n) from E's traces (before the E stage overwrites them)
-    if (HF && (r = dgm::launch_hf(c, TE, HF, nullptr, dt, st)) != DGM_OK) break;
-    if (h_done && s == nsteps - 1) cudaEventRecord(h_done, st);
+    if (HF && (q = dgm::launch_hf(c, TE, HF, nullptr, dt, ss)) != DGM_OK) return q;
+    if (h_done && last) cudaEventRecord(h_done, ss);
     double *TH = c->d_tr[2 + ch], *TEw = c->d_tr[up ? 1 - ce : ce];
     c->cur_HF = HF;
-    r = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, st);
+    q = dgm::launch_tb_stage(c, dgm::STAGE_E, H, E, nullptr, dt, 1, 1, dgm::OUT_UPDATE, TH, c->d_tr[ce], TEw, ss);
     c->cur_HF = nullptr;
     if (up) ce = 1 - ce;
+    return q;
+  };
+  int64_t s = 0;
+  // Long runs: replay a captured CUDA graph of kGraphSteps steps (an even count, so
+  // the upwind trace-buffer parities return to where they started and one graph
+  // serves every chunk).  Small meshes are launch-bound; the graph removes the
+  // per-kernel launch cost.  Same kernels, same order: bit-identical results.
+  constexpr int64_t kGraphSteps = 32;
+  const bool graphs = c->use_graphs && !h_done && nsteps >= 2 * kGraphSteps && r == DGM_OK;
+  if (graphs) {
+    const GraphKey key{E, H, HF, dt, ce, ch};
+    if (!c->gexec || !(c->gkey == key)) {
+      if (c->gexec) cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+      if (!c->gstream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+      const int ce0 = ce, ch0 = ch;
+      const int64_t l0 = c->launches;
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(c, cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeThreadLocal));
+      for (int64_t k = 0; k < kGraphSteps && r == DGM_OK; ++k) r = one_step(c->gstream, false);
+      cudaError_t ec = cudaStreamEndCapture(c->gstream, &g);
+      if (r != DGM_OK) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+      }
+      if (ec != cudaSuccess) return dgm::set_err(c, DGM_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+      ec = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (ec != cudaSuccess) return dgm::set_err(c, DGM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ec));
+      c->gkey = key;
+      c->glaunches = c->launches - l0;
+      c->launches = l0;
+      ce = ce0;
+      ch = ch0;
+    }
+    if (!c->gev[0]) {
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->gev[0], cudaEventDisableTiming));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->gev[1], cudaEventDisableTiming));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->gev[0], st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->gstream, c->gev[0], 0));
+    for (; s + kGraphSteps <= nsteps; s += kGraphSteps) {
+      CUDA_TRY(c, cudaGraphLaunch(c->gexec, c->gstream));
+      c->launches += c->glaunches;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->gev[1], c->gstream));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, c->gev[1], 0));
   }
+  for (; s < nsteps && r == DGM_OK; ++s) r = one_step(st, s == nsteps - 1);
   if (r == DGM_OK) {
     c->tr_valid = true;
     c->tr_E = E;

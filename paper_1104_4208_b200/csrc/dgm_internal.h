@@ -132,6 +132,17 @@ struct StageArgs {
 
 }  // namespace dgm
 
+// captured multi-step CUDA graph: valid for these field pointers, dt and the
+// trace-buffer parities at the start of a chunk
+struct GraphKey {
+  const double *E, *H, *HF;
+  double dt;
+  int ce, ch;
+  bool operator==(const GraphKey &o) const {
+    return E == o.E && H == o.H && HF == o.HF && dt == o.dt && ce == o.ce && ch == o.ch;
+  }
+};
+
 struct dgm_ctx {
   int p = 0, N = 0, NF = 0, LD = 0;
   int64_t n_tet = 0;
@@ -145,6 +156,12 @@ struct dgm_ctx {
   void *d_dense = nullptr;
   dgm::DevStream stream{};
   void *d_stream = nullptr;
+  int use_graphs = 1;                 // long dgm_step runs replay a captured graph (DGM_GRAPHS=0: off)
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  int64_t glaunches = 0;              // kernel launches per captured chunk
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev[2] = {nullptr, nullptr};
   std::vector<int32_t> nbr;
   std::vector<int8_t> nbrf, sign, bc;
   std::vector<dgm::Geo> h_geo;

@@ -148,3 +148,21 @@ def test_stab_cavity_resonances_through_library(engine):
     assert nz[:3] == pytest.approx([2 * np.pi ** 2] * 3, rel=2e-3)
     assert nz[3:5] == pytest.approx([3 * np.pi ** 2] * 2, rel=2e-3)
     assert nz[5:11] == pytest.approx([5 * np.pi ** 2] * 6, rel=1e-2)
+
+
+def test_stab_graph_replay_matches_single_steps():
+    """The captured-graph path of dgm_step_sc (100 steps) gives the same bits as
+    single-step continue calls, including the H^F update."""
+    import torch
+    from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
+    m, c, B, E, H, HF = _case(3, (True,) * 3, 3, seed=11)
+    dt = 1e-3
+    E1, H1 = _dev(c, E), _dev(c, H)
+    F1 = torch.as_tensor(HF, device="cuda").contiguous()
+    c.dgm_step_sc(E1, H1, F1, dt, 100)
+    E2, H2 = _dev(c, E), _dev(c, H)
+    F2 = torch.as_tensor(HF, device="cuda").contiguous()
+    c.dgm_step_sc(E2, H2, F2, dt, 1)
+    for _ in range(99):
+        c.dgm_step_sc(E2, H2, F2, dt, 1, DGM_STEP_CONTINUE)
+    assert bool((E1 == E2).all()) and bool((H1 == H2).all()) and bool((F1 == F2).all())
