@@ -130,7 +130,9 @@ dgm_status dgm_apply_flux(dgm_ctx *ctx, const double *E, const double *H, double
 /* nsteps of the symplectic-Euler map (reading G7: H staggered)
  *   H ← H + dt Ḣ(E, H);   E ← E + dt Ė(H, E)
  * in place on the device arrays E, H.  Upwind self-terms use the current value
- * of the field being updated.  DGM_EINVAL for a DGM_FLUX_STABILIZED context
+ * of the field being updated.  Calls of >= 64 steps replay a CUDA graph of 32
+ * captured steps (same kernels and order, bit-identical; DGM_GRAPHS=0 disables).
+ * DGM_EINVAL for a DGM_FLUX_STABILIZED context
  * (its state includes H^F: use dgm_step_sc); the same holds for dgm_step_ex and
  * dgm_step_host.  dgm_apply_flux and dgm_spectral_radius on such a context act
  * with the central flux alone (H^F = 0). */
