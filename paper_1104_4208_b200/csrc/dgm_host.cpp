@@ -633,7 +633,6 @@ dgm_status upload_impl(dgm_ctx *c) {
   int dev = 0;
   CUDA_TRY(c, cudaGetDevice(&dev));
   CUDA_TRY(c, cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev));
-  if (const char *v = std::getenv("DGM_HO_STREAM")) c->ho_stream = std::atoi(v) != 0;
   if (const char *v = std::getenv("DGM_GRAPHS")) c->use_graphs = std::atoi(v) != 0;
   CUDA_TRY(c, cudaMalloc(&c->d_geo, sizeof(Geo) * n));
   CUDA_TRY(c, cudaMemcpy(c->d_geo, c->h_geo.data(), sizeof(Geo) * n, cudaMemcpyHostToDevice));
@@ -669,7 +668,6 @@ dgm_status upload_impl(dgm_ctx *c) {
   }
   const HostProgSet &hs = kHostProgs[p - 1];
   size_t bytes = prog_bytes(hs.curl) + 256 + (size_t)c->N * 8;
-  for (int f = 0; f < 4; ++f) bytes += prog_bytes(hs.trace[f]) + prog_bytes(hs.lift[f]);
   for (int f = 0; f < 4; ++f)
     bytes += prog_bytes(hs.strace[f].prog) + prog_bytes(hs.slift[f].prog) + 2 * (((size_t)c->N * 2 + 255) & ~size_t(255));
   std::vector<char> buf(bytes, 0);
@@ -677,10 +675,6 @@ dgm_status upload_impl(dgm_ctx *c) {
   size_t off = 0;
   char *base = (char *)c->d_blob;
   c->progs.curl = stage_prog(hs.curl, buf, off, base);
-  for (int f = 0; f < 4; ++f) {
-    c->progs.trace[f] = stage_prog(hs.trace[f], buf, off, base);
-    c->progs.lift[f] = stage_prog(hs.lift[f], buf, off, base);
-  }
   auto stage_sprog = [&](const dgm::HostSProg &h, int nout) {
     dgm::DevSProg d;
     d.prog = stage_prog(h.prog, buf, off, base);

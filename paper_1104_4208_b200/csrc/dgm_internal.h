@@ -97,8 +97,6 @@ struct DenseOps {
 
 struct DevProgs {
   DevProg curl;
-  DevProg trace[4];
-  DevProg lift[4];
   DevSProg strace[4];
   DevSProg slift[4];
   const double *__restrict__ norms;
@@ -148,7 +146,6 @@ struct dgm_ctx {
   int64_t n_tet = 0;
   int flux = 0;
   int sms = 0;
-  int ho_stream = 1;   // sparse, p > kLanePmax: streamed-table kernels (DGM_HO_STREAM=0: one-element CTA kernels)
   int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
   int mixed = 0;       // 1: H ∈ P^{p-1} (E ∈ P^p), dense engine only; NH = N(p-1)
   int NH = 0;

@@ -1,8 +1,7 @@
-// High-order (p > kLanePmax) stage kernels for sm_100a (FP64), the trace-buffer
-// launchers for all orders, and the reductions (energy, mass inner product).
-//
-// A CTA of W warps owns one element at a time (grid-stride); its workspace lives
-// in shared memory.  Per element a stage does:
+// Stage dispatch for all orders and engines (lane-pair p <= kLanePmax, streamed
+// tables above, dense engine), the stabilised-flux face kernels, and the reductions
+// (energy, mass inner product).  Per element a stage does (SURVEY.md §8(a) S1-S6,
+// DESIGN.md §6):
 //   S1  reference curl of Ŷ by the sparse recurrence sweeps (level-scheduled
 //       pull-form program from gen/plan.py)
 //   S3  own and neighbour tangential traces of Ŷ read from the trace buffer
@@ -27,347 +26,6 @@ struct Dim {
   static constexpr int NF = (P + 1) * (P + 2) / 2;
   static constexpr int LD = (N + 3) & ~3;
 };
-
-// warp path with trace buffers: slots [0,9N) sweep (Ŷ then u), acc at 9N, A/B at 12N
-template <int P>
-struct Dim2 {
-  static constexpr int N = (P + 1) * (P + 2) * (P + 3) / 6;
-  static constexpr int NF = (P + 1) * (P + 2) / 2;
-  static constexpr int LD = (N + 3) & ~3;
-  static constexpr int ACC = 9 * N;   // must match gen/plan.py
-  static constexpr int SAB = 12 * N;
-  static constexpr int SCR = (3 * N + 1) & ~1;   // trace/lift scratch (pairs, 16-B aligned) in the dead sweep region
-  static constexpr int WS = 12 * N + 2 * NF;   // doubles per CTA (one element)
-  static constexpr int W = 4;                  // warps per CTA sharing the element
-};
-
-// Reference face tangents t̂1 = v̂b - v̂a, t̂2 = v̂c - v̂a (reading G9).
-__constant__ double kT1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
-__constant__ double kT2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
-
-// tangential components a1, a2 of mode a on reference face F
-template <int F>
-__device__ __forceinline__ void tangential(const double *sY, int N, int a, double &a1, double &a2) {
-  if (F == 0) {
-    double y0 = sY[a];
-    a1 = sY[N + a] - y0;
-    a2 = sY[2 * N + a] - y0;
-  } else if (F == 1) {
-    a1 = sY[N + a];
-    a2 = sY[2 * N + a];
-  } else if (F == 2) {
-    a1 = sY[a];
-    a2 = sY[2 * N + a];
-  } else {
-    a1 = sY[a];
-    a2 = sY[N + a];
-  }
-}
-
-__device__ __forceinline__ void ldterm(const DevProg &p, int q, double &cf, int &src) {
-  const double2 v = __ldg(p.term + q);
-  cf = v.x;
-  src = (int)__double_as_longlong(v.y);
-}
-
-// CTA-cooperative program execution for the high-order path: the W warps of a
-// CTA share one element workspace and split each DAG level's passes of 32 rows;
-// levels are separated by CTA barriers (all threads see the same sync flags).
-template <int W>
-__device__ __forceinline__ void cta_assign(const DevProg &p, double *s, int warp, int lane) {
-  int ps = 0;
-  while (ps < p.npass) {
-    int pe = ps;
-    while (!__ldg(p.sync + pe)) ++pe;               // last pass of this level
-    for (int q = ps + warp; q <= pe; q += W) {
-      const int row = q * 32 + lane;
-      const unsigned d = __ldg(p.dst + row);
-      if (d != 0xFFFFu) {
-        const int c = __ldg(p.cnt + row);
-        const int o = __ldg(p.off + q) * 32 + lane;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int t = 0; t < c; ++t) {
-          double cf;
-          int sr;
-          ldterm(p, o + 32 * t, cf, sr);
-          acc = fma(cf, s[sr], acc);
-        }
-        s[d] = acc;
-      }
-    }
-    __syncthreads();
-    ps = pe + 1;
-  }
-}
-
-// Staged (sum-factorised) trace of face F for both tangential components: stage 0
-// reads the volume field through tangential<F>, later stages the scratch (pairs);
-// the outputs are copied to out[0..NF) (k=1) and out[NF..2NF) (k=2).
-template <int F, int W>
-__device__ __forceinline__ void cta_strace_f(const DevSProg &sp, const double *sY, int N, int NF, double *scr,
-                                             double *out, int warp, int lane) {
-  const DevProg &p = sp.prog;
-  int ps = 0, lvl = 0;
-  while (ps < p.npass) {
-    int pe = ps;
-    while (!__ldg(p.sync + pe)) ++pe;
-    for (int q = ps + warp; q <= pe; q += W) {
-      const int row = q * 32 + lane;
-      const unsigned d = __ldg(p.dst + row);
-      if (d != 0xFFFFu) {
-        const int c = __ldg(p.cnt + row);
-        const int o = __ldg(p.off + q) * 32 + lane;
-        double t1 = 0.0, t2 = 0.0;
-        if (lvl == 0) {
-#pragma unroll 4
-          for (int t = 0; t < c; ++t) {
-            double cf, a1, a2;
-            int sr;
-            ldterm(p, o + 32 * t, cf, sr);
-            tangential<F>(sY, N, sr, a1, a2);
-            t1 = fma(cf, a1, t1);
-            t2 = fma(cf, a2, t2);
-          }
-        } else {
-#pragma unroll 4
-          for (int t = 0; t < c; ++t) {
-            double cf;
-            int sr;
-            ldterm(p, o + 32 * t, cf, sr);
-            const double2 v = *reinterpret_cast<const double2 *>(scr + 2 * sr);
-            t1 = fma(cf, v.x, t1);
-            t2 = fma(cf, v.y, t2);
-          }
-        }
-        *reinterpret_cast<double2 *>(scr + 2 * d) = make_double2(t1, t2);
-      }
-    }
-    __syncthreads();
-    ps = pe + 1;
-    ++lvl;
-  }
-  for (int g = warp * 32 + lane; g < NF; g += W * 32) {
-    const int sl = __ldg(sp.out + g);
-    out[g] = scr[2 * sl];
-    out[NF + g] = scr[2 * sl + 1];
-  }
-  __syncthreads();
-}
-
-template <int W>
-__device__ __forceinline__ void cta_strace(const DevProgs &pr, int f, const double *sY, int N, int NF, double *scr,
-                                           double *out, int warp, int lane) {
-  switch (f) {
-    case 0: cta_strace_f<0, W>(pr.strace[0], sY, N, NF, scr, out, warp, lane); break;
-    case 1: cta_strace_f<1, W>(pr.strace[1], sY, N, NF, scr, out, warp, lane); break;
-    case 2: cta_strace_f<2, W>(pr.strace[2], sY, N, NF, scr, out, warp, lane); break;
-    default: cta_strace_f<3, W>(pr.strace[3], sY, N, NF, scr, out, warp, lane); break;
-  }
-}
-
-// Staged lift of the two face fields A = AB[0..NF), B = AB[NF..2NF) into the
-// accumulator: acc[m][β] += t̂1_m L_f(A)_β + t̂2_m L_f(B)_β.
-template <int W>
-__device__ __forceinline__ void cta_slift2(const DevSProg &sp, const double *AB, int N, int NF, double *scr,
-                                           double *acc, int f, int warp, int lane) {
-  const DevProg &p = sp.prog;
-  int ps = 0, lvl = 0;
-  while (ps < p.npass) {
-    int pe = ps;
-    while (!__ldg(p.sync + pe)) ++pe;
-    for (int q = ps + warp; q <= pe; q += W) {
-      const int row = q * 32 + lane;
-      const unsigned d = __ldg(p.dst + row);
-      if (d != 0xFFFFu) {
-        const int c = __ldg(p.cnt + row);
-        const int o = __ldg(p.off + q) * 32 + lane;
-        double la = 0.0, lb = 0.0;
-        if (lvl == 0) {
-#pragma unroll 4
-          for (int t = 0; t < c; ++t) {
-            double cf;
-            int sr;
-            ldterm(p, o + 32 * t, cf, sr);
-            la = fma(cf, AB[sr], la);
-            lb = fma(cf, AB[NF + sr], lb);
-          }
-        } else {
-#pragma unroll 4
-          for (int t = 0; t < c; ++t) {
-            double cf;
-            int sr;
-            ldterm(p, o + 32 * t, cf, sr);
-            const double2 v = *reinterpret_cast<const double2 *>(scr + 2 * sr);
-            la = fma(cf, v.x, la);
-            lb = fma(cf, v.y, lb);
-          }
-        }
-        *reinterpret_cast<double2 *>(scr + 2 * d) = make_double2(la, lb);
-      }
-    }
-    __syncthreads();
-    ps = pe + 1;
-    ++lvl;
-  }
-  const double a0 = kT1[f][0], a1 = kT1[f][1], a2 = kT1[f][2];
-  const double b0 = kT2[f][0], b1 = kT2[f][1], b2 = kT2[f][2];
-  for (int b = warp * 32 + lane; b < N; b += W * 32) {
-    const int sl = __ldg(sp.out + b);
-    if (sl == 0xFFFF) continue;
-    const double la = scr[2 * sl], lb = scr[2 * sl + 1];
-    acc[b] += a0 * la + b0 * lb;
-    acc[N + b] += a1 * la + b1 * lb;
-    acc[2 * N + b] += a2 * la + b2 * lb;
-  }
-  __syncthreads();
-}
-
-template <int LD, int N>
-__device__ __forceinline__ void cta_load_elem(const double *__restrict__ F, int64_t e, int64_t cs, double *s, int tid,
-                                              int nthreads) {
-  for (int c = 0; c < 3; ++c) {
-    const double *src = F + c * cs + e * LD;
-    for (int i = tid; i < N; i += nthreads) s[c * N + i] = __ldg(src + i);
-  }
-}
-
-// High-order stage kernel (p > kLanePmax), trace-buffer scheme.  A CTA of W warps
-// owns one element at a time (grid-stride).  Own and neighbour traces of Ŷ come
-// from the trace buffer tr[e][f][k][γ] written by the stage that last updated Ŷ;
-// the lift acts on the two face fields A = -sf D₂ (+ upwind), B = sf D₁ (+ upwind),
-// acc_m += t̂1_m L_f(A) + t̂2_m L_f(B); after the update the CTA writes the traces
-// of the updated field for the next stage.
-template <int P, bool UP>
-__global__ void __launch_bounds__(Dim2<P>::W * 32)
-    stage2_kernel(StageArgs a, DevProgs pr, const double *__restrict__ trY, double *__restrict__ trOut) {
-  using D = Dim2<P>;
-  constexpr int N = D::N, NF = D::NF, LD = D::LD, W = D::W, NT = 32 * D::W;
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-  double *s = smem;
-  double *sACC = s + D::ACC;
-  double *sAB = s + D::SAB;
-  const int64_t cs = a.n_tet * LD;
-  const bool stageE = a.stage == STAGE_E;
-  const bool upd = a.out_mode == OUT_UPDATE;
-  const double mirrorY = stageE ? 1.0 : -1.0, mirrorX = stageE ? -1.0 : 1.0;
-  for (int64_t e = blockIdx.x; e < a.n_tet; e += gridDim.x) {
-    cta_load_elem<LD, N>(a.Y, e, cs, s, tid, NT);
-    __syncthreads();
-    if (a.do_curl) {
-      cta_assign<W>(pr.curl, s, warp, lane);
-    } else {
-      for (int i = tid; i < 3 * N; i += NT) sACC[i] = 0.0;
-      __syncthreads();
-    }
-    // Ŷ is dead (traces come from the buffer): stage X in its slots
-    if (upd) cta_load_elem<LD, N>(a.X, e, cs, s, tid, NT);
-    const Geo g = a.geo[e];
-    if (a.do_flux) {
-      const double sgn = g.detF > 0 ? 1.0 : -1.0;
-      for (int f = 0; f < 4; ++f) {
-        const int nb = a.nbr[4 * e + f];
-        const int gf = a.nbrf[4 * e + f];
-        double w = 0.5, kk = 0.0;
-        if (UP) {
-          const double Zm = g.Z, Zp = nb >= 0 ? a.geo[nb].Z : Zm;
-          if (stageE) {
-            w = Zp / (Zm + Zp);
-            kk = 1.0 / (Zm + Zp);
-          } else {
-            const double Ym = 1.0 / Zm, Yp = 1.0 / Zp;
-            w = Yp / (Ym + Yp);
-            kk = 1.0 / (Ym + Yp);
-          }
-        }
-        const double sf = (f & 1) ? -1.0 : 1.0;
-        const double *to = trY + (e * 4 + f) * 2 * NF;
-        const double *tn = nb >= 0 ? trY + ((int64_t)nb * 4 + gf) * 2 * NF : nullptr;
-        for (int gm = tid; gm < NF; gm += NT) {
-          const double o1 = __ldg(to + gm), o2 = __ldg(to + NF + gm);
-          const double n1 = nb >= 0 ? __ldg(tn + gm) : mirrorY * o1;
-          const double n2 = nb >= 0 ? __ldg(tn + NF + gm) : mirrorY * o2;
-          double h1 = 0.0, h2 = 0.0;   // stabilised flux (E stage): Δ_k -= H^F_k
-          if (a.HF) {
-            const double *hf = a.HF + (int64_t)a.fid[4 * e + f] * 2 * NF;
-            h1 = __ldg(hf + gm);
-            h2 = __ldg(hf + NF + gm);
-          }
-          double A = -sf * (w * (n2 - o2) - h2), B = sf * (w * (n1 - o1) - h1);
-          if (UP) {
-            const double *xo = a.trX + (e * 4 + f) * 2 * NF;
-            const double xo1 = __ldg(xo + gm), xo2 = __ldg(xo + NF + gm);
-            double xn1, xn2;
-            if (nb >= 0) {
-              const double *xn = a.trX + ((int64_t)nb * 4 + gf) * 2 * NF;
-              xn1 = __ldg(xn + gm);
-              xn2 = __ldg(xn + NF + gm);
-            } else {
-              xn1 = mirrorX * xo1;
-              xn2 = mirrorX * xo2;
-            }
-            const double j1 = kk * (xn1 - xo1), j2 = kk * (xn2 - xo2);
-            const double *M = a.fmet + 12 * e + 3 * f;
-            const double ps = (stageE ? 1.0 : -1.0) * sgn;
-            A += ps * (j1 * M[0] + j2 * M[1]);
-            B += ps * (j1 * M[1] + j2 * M[2]);
-          }
-          sAB[gm] = A;
-          sAB[NF + gm] = B;
-        }
-        __syncthreads();
-        cta_slift2<W>(pr.slift[f], sAB, N, NF, s + D::SCR, sACC, f, warp, lane);
-      }
-    }
-    // S2 + S6: inverse mass with geometry, then update (X staged in slots [0,3N)) or write
-    const double cm = stageE ? g.inv_eps : -g.inv_mu;
-    for (int b = tid; b < N; b += NT) {
-      const double v0 = sACC[b], v1 = sACC[N + b], v2 = sACC[2 * N + b];
-      const double x0 = cm * (g.g[0] * v0 + g.g[1] * v1 + g.g[2] * v2);
-      const double x1 = cm * (g.g[1] * v0 + g.g[3] * v1 + g.g[4] * v2);
-      const double x2 = cm * (g.g[2] * v0 + g.g[4] * v1 + g.g[5] * v2);
-      const int64_t o = e * LD + b;
-      if (upd) {
-        const double y0 = s[b] + a.dt * x0, y1 = s[N + b] + a.dt * x1, y2 = s[2 * N + b] + a.dt * x2;
-        s[b] = y0;
-        s[N + b] = y1;
-        s[2 * N + b] = y2;
-        a.X[o] = y0;
-        a.X[cs + o] = y1;
-        a.X[2 * cs + o] = y2;
-      } else if (a.out_mode == OUT_WRITE) {
-        a.dX[o] = x0;
-        a.dX[cs + o] = x1;
-        a.dX[2 * cs + o] = x2;
-      } else {
-        a.dX[o] += x0;
-        a.dX[cs + o] += x1;
-        a.dX[2 * cs + o] += x2;
-      }
-    }
-    __syncthreads();
-    if (upd && trOut)
-      for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, s, N, NF, s + D::SCR, trOut + (e * 4 + f) * 2 * NF, warp, lane);
-    __syncthreads();
-  }
-}
-
-// tangential traces of a field for all elements -> tr[e][f][k][γ] (high-order layout)
-template <int P>
-__global__ void __launch_bounds__(Dim2<P>::W * 32) trace2_kernel(const double *__restrict__ X, double *tr,
-                                                                  int64_t n_tet, DevProgs pr) {
-  using D = Dim2<P>;
-  constexpr int N = D::N, NF = D::NF, LD = D::LD, W = D::W, NT = 32 * D::W;
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t cs = n_tet * LD;
-  for (int64_t e = blockIdx.x; e < n_tet; e += gridDim.x) {
-    cta_load_elem<LD, N>(X, e, cs, smem, threadIdx.x, NT);
-    __syncthreads();
-    for (int f = 0; f < 4; ++f) cta_strace<W>(pr, f, smem, N, NF, smem + D::SCR, tr + (e * 4 + f) * 2 * NF, warp, lane);
-  }
-}
 
 // Energy ½ Σ_T sgn(det F) Σ_α ‖φ_α‖² (ε Ê_αᵀ G'^{-1} Ê_α + μ Ĥ_αᵀ G'^{-1} Ĥ_α)
 // (|det F| F^{-1}F^{-T} = sgn G'^{-1}).  One thread
@@ -425,55 +83,6 @@ __global__ void sum_kernel(const double *partial, int n, double *out) {
 }
 
 // ---------------------------------------------------------------------------
-template <int P>
-static dgm_status launch_stage2_p(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st) {
-  using D = Dim2<P>;
-  const size_t smem = sizeof(double) * D::WS;
-  auto go = [&](auto kernel) {
-    int occ = 0;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, D::W * 32, smem);
-    if (occ < 1) occ = 1;
-    int64_t grid = (int64_t)c->sms * occ;
-    if (grid > c->n_tet) grid = c->n_tet;
-    kernel<<<(unsigned)grid, D::W * 32, smem, st>>>(a, c->progs, trY, trOut);
-  };
-  if (a.upwind) go(stage2_kernel<P, true>);
-  else go(stage2_kernel<P, false>);
-  c->launches++;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("stage2_kernel: ") + cudaGetErrorString(e));
-  return DGM_OK;
-}
-
-template <int P>
-static dgm_status launch_trace2_p(dgm_ctx *c, const double *X, double *tr, cudaStream_t st) {
-  using D = Dim2<P>;
-  const size_t smem = sizeof(double) * D::WS;
-  int occ = 0;
-  cudaFuncSetAttribute(trace2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace2_kernel<P>, D::W * 32, smem);
-  if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)c->sms * occ;
-  if (grid > c->n_tet) grid = c->n_tet;
-  trace2_kernel<P><<<(unsigned)grid, D::W * 32, smem, st>>>(X, tr, c->n_tet, c->progs);
-  c->launches++;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(c, DGM_ECUDA, std::string("trace2_kernel: ") + cudaGetErrorString(e));
-  return DGM_OK;
-}
-
-#define DGM_DISPATCH_HI(p, fn, ...)      \
-  switch (p) {                           \
-    case 5: return fn<5>(__VA_ARGS__);   \
-    case 6: return fn<6>(__VA_ARGS__);   \
-    case 7: return fn<7>(__VA_ARGS__);   \
-    case 8: return fn<8>(__VA_ARGS__);   \
-    case 9: return fn<9>(__VA_ARGS__);   \
-    case 10: return fn<10>(__VA_ARGS__); \
-    default: return DGM_EORDER;          \
-  }
-
 #define DGM_DISPATCH(p, fn, ...)          \
   switch (p) {                            \
     case 1: return fn<1>(__VA_ARGS__);    \
@@ -514,16 +123,14 @@ dgm_status launch_tb_stage(dgm_ctx *c, int stage, const double *Y, double *X, do
   a.do_flux = do_flux;
   a.out_mode = out_mode;
   if (c->engine == 1) return launch_dense_stage(c, a, trY, trOut, st);
-  if (c->ho_stream) return launch_stream_stage(c, a, trY, trOut, st);
-  DGM_DISPATCH_HI(c->p, launch_stage2_p, c, a, trY, trOut, st)
+  return launch_stream_stage(c, a, trY, trOut, st);
 }
 
 dgm_status launch_tb_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field) {
   if (c->n_tet == 0) return DGM_OK;
   if (c->engine == 1) return launch_dense_traces(c, X, tr, st, field);
   if (c->p <= kLanePmax) return launch_lane_traces(c, X, tr, st);
-  if (c->ho_stream) return launch_stream_traces(c, X, tr, st);
-  DGM_DISPATCH_HI(c->p, launch_trace2_p, c, X, tr, st)
+  return launch_stream_traces(c, X, tr, st);
 }
 
 // (A, M_m B) = Σ_T |det F| m_T Σ_α ‖φ_α‖² A_αᵀ F^{-1}F^{-T} B_α  (m = ε or μ), the
