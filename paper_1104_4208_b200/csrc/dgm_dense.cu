@@ -195,22 +195,23 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
-      const unsigned mask = (kcur >> (16 + 3 * wn)) & 7u;
+      const unsigned m12 = (kcur >> 16) & 0xFFFu;   // non-zero 16x8 column groups of this k-tile
       kcur = knext;
-      // skip the zero 16x32 blocks of the operator: a CTA-uniform branch around a
-      // whole column block, so the tensor pipe is not occupied by dead MMAs
+      // skip zero operator blocks: a CTA-uniform branch per 32-column block, then per
+      // 8-column group (whole 16-row k-tile each, so the tensor pipe is not occupied)
 #pragma unroll
       for (int grp = 0; grp < 3; ++grp) {
-        if (mask & (1u << grp)) {
+        if ((m12 >> (4 * grp)) & 0xFu) {
 #pragma unroll
-          for (int k4 = 0; k4 < BK / 4; ++k4) {
-            double b[4];
+          for (int jj = 0; jj < 4; ++jj) {
+            if ((m12 >> (4 * grp + jj)) & 1u) {
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) b[jj] = sm.B[st][k4 * 4 + gc][wn * BN + grp * 32 + jj * 8 + gr];
+              for (int k4 = 0; k4 < BK / 4; ++k4) {
+                const double b = sm.B[st][k4 * 4 + gc][wn * BN + grp * 32 + jj * 8 + gr];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-              for (int i = 0; i < 2; ++i) dmma(acc[grp * 4 + jj][i][0], acc[grp * 4 + jj][i][1], a[k4][i], b[jj]);
+                for (int i = 0; i < 2; ++i) dmma(acc[grp * 4 + jj][i][0], acc[grp * 4 + jj][i][1], a[k4][i], b);
+              }
+            }
           }
         }
       }

@@ -274,9 +274,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   };
   clean(B1);
   clean(B2);
-  // per n-tile: non-zero k-tiles with the mask of non-zero 16x32 column blocks
-  // (one per warp column of the GEMM CTA)
-  constexpr int GW = 32;
+  // per n-tile: non-zero k-tiles with the mask of non-zero 16x8 column groups
+  constexpr int GW = 8;   // 16x8 blocks (one MMA column group); 12 mask bits per k-tile
   auto tiles = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int klo, int khi,
                    std::vector<uint32_t> &ktl, std::vector<int32_t> &ktoff) {
     ktl.clear();
