@@ -1,3 +1,5 @@
+# Round-end verification on one B200 (run via gpurun): smoke, GPU tests, default bench,
+# reference arm, ncu launch list of the default bench, C3-C5 bench lines.
 cd $GRAFT_REPO_ROOT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -3
 timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -3
