@@ -102,6 +102,10 @@ class TierB:
 
     # --- the operator ----------------------------------------------------
     def dE(self, E, H, part="all"):
+        return self._apply_G(self.acc_E(E, H, part), 1.0 / self.eps)
+
+    def acc_E(self, E, H, part="all"):
+        """E-equation residual after the diagonal reference mass (before G'/ε)."""
         norms = self.R["norms"]
         acc = np.zeros((3, self.n_tet, self.N))
         if part in ("all", "curl"):
@@ -122,9 +126,13 @@ class TierB:
                 kE = (1.0 / (Zm + Zp))[:, :, None, None]
                 R += self.sgn[None, :, None] * self._lift_tan(kE * (Ep - trE))
             acc += R / norms[None, None, :]
-        return self._apply_G(acc, 1.0 / self.eps)
+        return acc
 
     def dH(self, E, H, part="all"):
+        return self._apply_G(self.acc_H(E, H, part), -1.0 / self.mu)
+
+    def acc_H(self, E, H, part="all"):
+        """H-equation residual after the diagonal reference mass (before -G'/μ)."""
         norms = self.R["norms"]
         acc = np.zeros((3, self.n_tet, self.N))
         if part in ("all", "curl"):
@@ -145,7 +153,7 @@ class TierB:
                 kH = (1.0 / (Ym + Yp))[:, :, None, None]
                 R -= self.sgn[None, :, None] * self._lift_tan(kH * (Hp - trH))
             acc += R / norms[None, None, :]
-        return self._apply_G(acc, -1.0 / self.mu)
+        return acc
 
     def energy(self, E, H):
         """½ Σ_T |det F| Σ_α ‖φ_α‖² (ε Ê_αᵀ G Ê_α + μ Ĥ_αᵀ G Ĥ_α), G = F^{-1}F^{-T}
@@ -400,3 +408,52 @@ class TierBMixed:
 
     def energy(self, E, H):
         return self.B.energy(E, self._h(H))
+
+
+class TierBVar(TierB):
+    """Intra-element variable ε(x), μ(x) on flat elements via the paper's "reverse
+    numerical integration" (NEXT-4, central flux).
+
+    With a non-constant coefficient the element mass ∫_T m(x) u·v is full.  The
+    paper keeps a diagonal mass by approximating ṽ = |det F| m v in the same basis
+    and evaluating the functional by quadrature: the residual r (given modally,
+    r_β = ∫ f φ_β) is represented pointwise through its modal expansion
+    f = Σ_α (r_α/‖φ_α‖²) φ_α ("reverse numerical integration"), divided by m at
+    the integration points, and integrated back.  For the covariant fields of the
+    E and H equations this gives, per element and covariant
+    component, the approximate inverse
+        Ẋ = G' · S(acc),   S(v)_β = (1/‖φ_β‖²) Σ_i ŵ_i φ_β(x̂_i) (1/m(x_i)) Σ_α φ_α(x̂_i) v_α
+    where acc is the residual after the diagonal reference mass (as in TierB) and
+    (x̂_i, ŵ_i) is the collapsed Gauss–Jacobi rule with p+2 points per direction.
+    For constant m, S = 1/m exactly (Φᵀ W Φ = diag ‖φ‖²), i.e. TierB.  The result is
+    symmetric positive definite in the appropriate inner product."""
+
+    def __init__(self, xyz, tet, rep, p, eps_fn, mu_fn):
+        super().__init__(xyz, tet, rep, p, 1.0, 1.0, "central")
+        from .basis import phi
+        from .jacobi import tet_rule
+        pts, w = tet_rule(p + 2)
+        self.Phi = phi(p, pts)                                   # [N, Q]
+        self.qw = w
+        X0 = np.asarray(xyz, dtype=np.float64)[np.asarray(tet)[:, 0]]   # [n, 3]
+        xq = X0[:, None, :] + np.einsum("tij,qj->tqi", self.F, pts)     # [n, Q, 3] physical points
+        self.xq = xq
+        self.inv_eps_q = 1.0 / np.asarray(eps_fn(xq.reshape(-1, 3)), dtype=np.float64).reshape(xq.shape[:2])
+        self.inv_mu_q = 1.0 / np.asarray(mu_fn(xq.reshape(-1, 3)), dtype=np.float64).reshape(xq.shape[:2])
+
+    def S(self, acc, inv_m_q):
+        """Reverse integration, 1/m at the points, integration back (per component)."""
+        vals = np.einsum("aq,lta->ltq", self.Phi, acc)
+        vals = vals * (self.qw[None, None, :] * inv_m_q[None, :, :])
+        return np.einsum("aq,ltq->lta", self.Phi, vals) / self.R["norms"][None, None, :]
+
+    def dE(self, E, H, part="all"):
+        return self._apply_G(self.S(self.acc_E(E, H, part), self.inv_eps_q), np.ones(self.n_tet))
+
+    def dH(self, E, H, part="all"):
+        return self._apply_G(self.S(self.acc_H(E, H, part), self.inv_mu_q), -np.ones(self.n_tet))
+
+    def mass_inverse_matrix(self, T, inv_m_q):
+        """The approximate inverse (per scalar component, element T) as an N×N matrix."""
+        W = self.qw * inv_m_q[T]
+        return (self.Phi * W[None, :]) @ self.Phi.T / self.R["norms"][:, None]
