@@ -102,6 +102,14 @@ typedef struct {
                             (AUTO resolves to it).  Both fields keep the order-`order`
                             layout; H's modes >= N(order-1) are ignored by the
                             operator and stay zero when zero on input.            */
+  int32_t material_points; /* 1: eps and mu point to [n_tet][Q] values at the
+                            element's quadrature points (dgm_quadrature_host;
+                            physical point x = X0 + F ξ).  The inverse mass is then
+                            the paper's "reverse numerical integration" approximate
+                            inverse: residual -> values at the
+                            points -> × ŵ_i / m(x_i) -> back to the modes.  Central
+                            flux, equal orders, dense engine (AUTO resolves to it);
+                            dgm_energy and dgm_spectral_radius are not available. */
 } dgm_opts;
 
 /* Validate the mesh, match faces, compute per-element geometry
@@ -216,6 +224,12 @@ dgm_status dgm_match_faces_host(const dgm_mesh *mesh, int32_t *nbr, int8_t *nbr_
 
 /* Number of kernel launches the last dgm_step/dgm_apply_* call enqueued. */
 int64_t dgm_last_launches(const dgm_ctx *ctx);
+
+/* Host-only: the reference quadrature of order-`order` contexts with material_points:
+ * the collapsed Gauss–Jacobi rule with order+2 points per direction (exact to degree
+ * 2·order+3), *Q points ξ_i (xi: [Q][3], may be NULL) and weights (w: [Q], may be
+ * NULL).  Point i of element T is X0_T + F_T ξ_i. */
+dgm_status dgm_quadrature_host(int order, int64_t *Q, double *xi, double *w);
 
 /* The engine the context resolved to (DGM_ENGINE_SPARSE or DGM_ENGINE_DENSE). */
 int dgm_engine(const dgm_ctx *ctx);

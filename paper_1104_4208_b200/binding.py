@@ -21,7 +21,7 @@ FLUX = {"central": 0, "upwind": 1, "stabilized": 2}
 ENGINE = {"auto": 0, "sparse": 1, "dense": 2}
 DGM_STEP_CONTINUE = 1
 EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
-           "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_engine", "dgm_last_error", "dgm_destroy"]
+           "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_engine", "dgm_quadrature_host", "dgm_last_error", "dgm_destroy"]
 
 
 class DgmError(RuntimeError):
@@ -37,7 +37,8 @@ class _Mesh(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32),
-                ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32), ("mixed_order", ctypes.c_int32)]
+                ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32), ("mixed_order", ctypes.c_int32),
+                ("material_points", ctypes.c_int32)]
 
 
 _lib = None
@@ -70,6 +71,7 @@ def load_library(path: str = LIB_PATH):
         "dgm_match_faces_host": (I32, [ctypes.POINTER(_Mesh), P, P, P, P]),
         "dgm_last_launches": (I64, [P]),
         "dgm_engine": (I32, [P]),
+        "dgm_quadrature_host": (I32, [I32, ctypes.POINTER(I64), P, P]),
         "dgm_last_error": (ctypes.c_char_p, [P]),
         "dgm_destroy": (None, [P]),
     }
@@ -89,6 +91,30 @@ def _stream(stream):
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def dgm_quadrature_host(order):
+    """(xi [Q,3], w [Q]): the reference quadrature used by material_points contexts."""
+    lib = load_library()
+    Q = ctypes.c_int64()
+    st = lib.dgm_quadrature_host(int(order), ctypes.byref(Q), None, None)
+    if st != DGM_OK:
+        raise DgmError(st, "bad order")
+    xi = np.empty((Q.value, 3))
+    w = np.empty(Q.value)
+    lib.dgm_quadrature_host(int(order), ctypes.byref(Q), xi.ctypes.data, w.ctypes.data)
+    return xi, w
+
+
+def material_at_points(xyz, tet, order, fn):
+    """[n_tet, Q] samples of fn(x) at the library's quadrature points x = X0 + F ξ."""
+    xyz = np.asarray(xyz, dtype=np.float64)
+    tet = np.asarray(tet)
+    xi, _ = dgm_quadrature_host(order)
+    X = xyz[tet]
+    F = np.stack([X[:, 1] - X[:, 0], X[:, 2] - X[:, 0], X[:, 3] - X[:, 0]], axis=2)
+    xq = X[:, 0][:, None, :] + np.einsum("tij,qj->tqi", F, xi)
+    return np.asarray(fn(xq.reshape(-1, 3)), dtype=np.float64).reshape(xq.shape[:2])
 
 
 def dgm_match_faces_host(xyz, tet, rep=None):
@@ -111,7 +137,7 @@ class Context:
     """Owns a dgm_ctx.  Methods mirror the C ABI names (dgm_*)."""
 
     def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0, engine="auto",
-                 mixed_order=False):
+                 mixed_order=False, material_points=False):
         lib = load_library()
         self._lib = lib
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
@@ -122,8 +148,15 @@ class Context:
         self._keep = (xyz, tet, repa, eps_a, mu_a)
         m = _Mesh(xyz.shape[0], xyz.ctypes.data, tet.shape[0], tet.ctypes.data,
                   None if repa is None else repa.ctypes.data)
+        if material_points:   # eps, mu: [n_tet, Q] values at the quadrature points
+            eps_a = np.ascontiguousarray(np.asarray(eps, dtype=np.float64).ravel())
+            mu_a = np.ascontiguousarray(np.asarray(mu, dtype=np.float64).ravel())
+            nq = tet.shape[0] * dgm_quadrature_host(p)[1].size
+            if eps_a.size != nq or mu_a.size != nq:
+                raise ValueError(f"material_points: eps and mu must hold n_tet*Q = {nq} values")
+            self._keep = (xyz, tet, repa, eps_a, mu_a)
         o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0), ENGINE[engine],
-                  int(bool(mixed_order)))
+                  int(bool(mixed_order)), int(bool(material_points)))
         # H's live modes: N(p-1) for mixed orders (E ∈ P^p, H ∈ P^{p-1}), else N
         self.NH = p * (p + 1) * (p + 2) // 6 if mixed_order else (p + 1) * (p + 2) * (p + 3) // 6
         h = ctypes.c_void_p()

@@ -70,6 +70,7 @@ struct GemmArgs {
   const int32_t *ktoff;
   int ntiles_n;
   int64_t n_tet;
+  int Na;                  // valid rows per A block (k < k1): N, or Q for point values
   // epilogue
   int N, NF, LD;
   int ncols;   // valid output columns (EPI_TRACE: 8NF)
@@ -77,6 +78,14 @@ struct GemmArgs {
   double *X, *dX, *tr;
   double dt;
   int stageE, out_mode;
+  // variable materials (reverse numerical integration): EPI_TRACE scales column
+  // c*sQ + i by scale[e*sQ + i]; EPI_STAGE with raw != null writes the residual
+  // v_c(β) to raw[e*rawld + c*rawNk + β] instead of updating; unit_m: cm = ±1
+  const double *scale;
+  int sQ;
+  double *raw;
+  int rawld, rawNk;
+  int unit_m;
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -110,7 +119,7 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
   if (lo) {
     blk = k0 / g.Nk;
     q0 = k0 - blk * g.Nk;
-    lim = g.N;
+    lim = g.Na;
   } else {
     blk = (k0 - g.k1) / g.NFk;
     q0 = (k0 - g.k1) - blk * g.NFk;
@@ -228,10 +237,16 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
           const int col = n0 + wn * BN + j * 8 + 2 * gc;
+          double v0 = acc[j][i][0], v1 = acc[j][i][1];
+          if (g.scale) {   // point values: quadrature weight / material at the point
+            const double *sc = g.scale + e * g.sQ;
+            v0 *= col < g.ncols ? sc[col % g.sQ] : 0.0;
+            v1 *= col + 1 < g.ncols ? sc[(col + 1) % g.sQ] : 0.0;
+          }
           if (col + 1 < g.ncols) {
-            *reinterpret_cast<double2 *>(row + col) = make_double2(acc[j][i][0], acc[j][i][1]);
+            *reinterpret_cast<double2 *>(row + col) = make_double2(v0, v1);
           } else if (col < g.ncols) {
-            row[col] = acc[j][i][0];
+            row[col] = v0;
           }
         }
       }
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const Geo &G = g.geo[e];
 #pragma unroll
           for (int q = 0; q < 6; ++q) Gs[r][q] = G.g[q];
-          Gs[r][6] = g.stageE ? G.inv_eps : -G.inv_mu;
+          Gs[r][6] = g.unit_m ? (g.stageE ? 1.0 : -1.0) : (g.stageE ? G.inv_eps : -G.inv_mu);
         }
       }
       __syncthreads();
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           o[u] = (idx < BM * MODES && e < g.n_tet && b < g.N) ? e * g.LD + b : -1;
 #pragma unroll
           for (int cc = 0; cc < 3; ++cc)
-            xv[u][cc] = (o[u] >= 0 && g.out_mode != OUT_WRITE) ? out[cc * cs + o[u]] : 0.0;
+            xv[u][cc] = (o[u] >= 0 && g.out_mode != OUT_WRITE && !g.raw) ? out[cc * cs + o[u]] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -286,6 +301,13 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const double cm = G[6];
           const int hb = (ml >> 5) * BN + (ml & 31);
           const double v0 = Cs[r][hb], v1 = Cs[r][32 + hb], v2 = Cs[r][64 + hb];
+          if (g.raw) {   // residual before the (variable-material) inverse mass
+            double *rw = g.raw + (m0 + r) * (int64_t)g.rawld + 32 * NH * nt + ml;
+            rw[0] = v0;
+            rw[g.rawNk] = v1;
+            rw[2 * g.rawNk] = v2;
+            continue;
+          }
           const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
           const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
           const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
@@ -447,8 +469,54 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.dt = a.dt;
   g.stageE = a.stage == STAGE_E;
   g.out_mode = a.out_mode;
-  dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
-  if (s != DGM_OK) return s;
+  g.Na = c->N;
+  if (c->matq) {
+    // variable materials: write the residual, then the reverse-numerical-integration
+    // inverse mass as two more GEMMs: residual -> point values ×
+    // ŵ_i/m(x_i), point values -> modes (1/‖φ‖²), then G' and the update
+    const int Nk = D.k1a / 3, Qk = c->Qk;
+    g.raw = D.AC;
+    g.rawld = 3 * Nk;
+    g.rawNk = Nk;
+    dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
+    if (s != DGM_OK) return s;
+    GemmArgs f{};
+    f.p0 = f.p1 = D.AC;
+    f.ld0 = f.ld1 = 3 * Nk;
+    f.cs = Nk;
+    f.k1 = 1 << 30;
+    f.Nk = Nk;
+    f.NFk = Nk;
+    f.Na = c->N;
+    f.Bm = D.Bf;
+    f.NC = D.ncf;
+    f.ktl = D.ktlf;
+    f.ktoff = D.ktofff;
+    f.ntiles_n = D.ncf / BNT;
+    f.n_tet = c->n_tet;
+    f.ncols = 3 * Qk;
+    f.tr = D.P;
+    f.scale = a.stage == STAGE_E ? D.SWe : D.SWm;
+    f.sQ = Qk;
+    if ((s = gemm_go<EPI_TRACE>(c, f, st)) != DGM_OK) return s;
+    GemmArgs b = g;
+    b.raw = nullptr;
+    b.p0 = b.p1 = D.P;
+    b.ld0 = b.ld1 = 3 * Qk;
+    b.cs = Qk;
+    b.k1 = 1 << 30;
+    b.Nk = Qk;
+    b.NFk = Qk;
+    b.Na = c->Q;
+    b.Bm = D.Bb;
+    b.ktl = D.ktlb;
+    b.ktoff = D.ktoffb;
+    b.unit_m = 1;
+    if ((s = gemm_go<EPI_STAGE>(c, b, st)) != DGM_OK) return s;
+  } else {
+    dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
+    if (s != DGM_OK) return s;
+  }
   if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st, v);
   return DGM_OK;
 }
@@ -463,6 +531,7 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
   g.k1 = 1 << 30;
   g.Nk = D.k1a / 3;
   g.NFk = (c->NF + BK - 1) / BK * BK;
+  g.Na = c->N;
   g.Bm = D.B2[field];
   g.NC = D.nc2;
   g.ktl = D.ktl2[field];

@@ -172,6 +172,93 @@ dgm_status build_stream(dgm_ctx *c, const HostProgSet &hs, size_t chunk_cap) {
   return DGM_OK;
 }
 
+// ---- reverse numerical integration (variable materials inside elements) -------
+// Jacobi P_n^{(a,0)}(x) and its derivative by the three-term recurrence.
+void jacobi_pd(int n, double a, double x, double &P, double &dP) {
+  double p0 = 1.0, p1 = 0.5 * (a + (a + 2.0) * x);   // P_1^{(a,0)} = (a + (a+2) x)/2
+  double d0 = 0.0, d1 = 0.5 * (a + 2.0);
+  if (n == 0) {
+    P = 1.0;
+    dP = 0.0;
+    return;
+  }
+  for (int k = 2; k <= n; ++k) {
+    const double kk = k, c = 2.0 * kk + a;
+    const double A = 2.0 * kk * (kk + a) * (c - 2.0);
+    const double B = (c - 1.0) * (c * (c - 2.0) * x + a * a);
+    const double C = 2.0 * (kk + a - 1.0) * (kk - 1.0) * c;
+    const double p2 = (B * p1 - C * p0) / A;
+    const double d2 = (B * d1 + (c - 1.0) * c * (c - 2.0) * p1 - C * d0) / A;
+    p0 = p1;
+    p1 = p2;
+    d0 = d1;
+    d1 = d2;
+  }
+  P = p1;
+  dP = d1;
+}
+// q-point Gauss–Jacobi rule for the weight (1-x)^a on [-1,1]: Newton on the zeros of
+// P_q^{(a,0)} with deflation, weights 2^{a+1} / ((1-x²) P'(x)²).
+void gauss_jacobi(int q, double a, std::vector<double> &x, std::vector<double> &w) {
+  x.assign(q, 0.0);
+  w.assign(q, 0.0);
+  for (int k = 0; k < q; ++k) {
+    double r = -std::cos((2.0 * k + 1.0) * M_PI / (2.0 * q));   // Chebyshev guess
+    if (k > 0) r = 0.5 * (r + x[k - 1]);
+    for (int it = 0; it < 100; ++it) {
+      double P, dP;
+      jacobi_pd(q, a, r, P, dP);
+      double s = 0.0;
+      for (int i = 0; i < k; ++i) s += 1.0 / (r - x[i]);
+      const double delta = -P / (dP - s * P);
+      r += delta;
+      if (std::fabs(delta) < 1e-16) break;
+    }
+    x[k] = r;
+  }
+  for (int k = 0; k < q; ++k) {
+    double P, dP;
+    jacobi_pd(q, a, x[k], P, dP);
+    w[k] = std::pow(2.0, a + 1.0) / ((1.0 - x[k] * x[k]) * dP * dP);
+  }
+}
+// Collapsed rule on the reference tet (q = p+2 per direction, exact to degree 2q-1):
+// x = (1+a)/2, y = (1-a)(1+b)/4, z = (1-a)(1-b)(1+c)/8, weights (2,0),(1,0),(0,0) / 64.
+void tet_quadrature(int p, std::vector<double> &xi, std::vector<double> &w) {
+  const int q = p + 2;
+  std::vector<double> a, wa, b, wb, c, wc;
+  gauss_jacobi(q, 2.0, a, wa);
+  gauss_jacobi(q, 1.0, b, wb);
+  gauss_jacobi(q, 0.0, c, wc);
+  xi.clear();
+  w.clear();
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j)
+      for (int k = 0; k < q; ++k) {
+        xi.push_back(0.5 * (1.0 + a[i]));
+        xi.push_back(0.25 * (1.0 - a[i]) * (1.0 + b[j]));
+        xi.push_back(0.125 * (1.0 - a[i]) * (1.0 - b[j]) * (1.0 + c[k]));
+        w.push_back(wa[i] * wb[j] * wc[k] / 64.0);
+      }
+}
+// φ_ijk(x,y,z) = (1-x-y)^i (1-x)^j P_i(2z/(1-x-y)-1) P_j^{(2i+1,0)}(2y/(1-x)-1)
+//               P_k^{(2i+2j+2,0)}(2x-1), graded ABI mode order.
+void basis_at(int p, const double *pt, double *out) {
+  const double x = pt[0], y = pt[1], z = pt[2];
+  const double s = 1.0 - x - y, r = 1.0 - x;
+  int m = 0;
+  for (int n = 0; n <= p; ++n)
+    for (int i = 0; i <= n; ++i)
+      for (int j = 0; j <= n - i; ++j) {
+        const int k = n - i - j;
+        double Pi, Pj, Pk, d;
+        jacobi_pd(i, 0.0, 2.0 * z / s - 1.0, Pi, d);
+        jacobi_pd(j, 2.0 * i + 1.0, 2.0 * y / r - 1.0, Pj, d);
+        jacobi_pd(k, 2.0 * i + 2.0 * j + 2.0, 2.0 * x - 1.0, Pk, d);
+        out[m++] = std::pow(s, i) * std::pow(r, j) * Pi * Pj * Pk;
+      }
+}
+
 // ---- dense engine: assemble the operator matrices from the exact programs ------
 // Scalar executor of an ELL program (passes in order respect the DAG levels).
 void exec_prog_host(const HostProg &hp, std::vector<double> &s) {
@@ -210,6 +297,8 @@ void exec_staged_host(const dgm::HostSProg &sp, const std::vector<double> &in, s
   out.assign(nout, 0.0);
   for (int i = 0; i < nout; ++i) out[i] = sp.out[i] == 0xFFFF ? 0.0 : scr[sp.out[i]];
 }
+
+int64_t n_or1(const dgm_ctx *c) { return c->n_tet > 0 ? c->n_tet : 1; }
 
 dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   constexpr int BK = 16, BN = 96;
@@ -379,6 +468,42 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   D.nc1 = nc1;
   D.nc2 = nc2;
   D.k1a = k1a;
+  if (c->matq) {
+    // reverse numerical integration: residual (component-blocked, Nk rows) -> point
+    // values (Qk per component) -> weighted by ŵ_i/m(x_i) -> back to modes with
+    // 1/‖φ‖², columns in the B1 output layout m*Np + β
+    const int Q = c->Q, Qk = c->Qk;
+    std::vector<double> xi, w;
+    tet_quadrature(c->p, xi, w);
+    std::vector<double> Phi((size_t)Q * N);
+    for (int i = 0; i < Q; ++i) basis_at(c->p, &xi[3 * i], &Phi[(size_t)i * N]);
+    const int ncf = (3 * Qk + BNT - 1) / BNT * BNT;
+    std::vector<double> Bf((size_t)3 * Nk * ncf, 0.0), Bb((size_t)3 * Qk * nc1, 0.0);
+    for (int cc = 0; cc < 3; ++cc)
+      for (int b = 0; b < N; ++b)
+        for (int i = 0; i < Q; ++i) {
+          Bf[(size_t)(cc * Nk + b) * ncf + cc * Qk + i] = Phi[(size_t)i * N + b];
+          Bb[(size_t)(cc * Qk + i) * nc1 + (size_t)cc * Np + b] = Phi[(size_t)i * N + b] / hs.norms[b];
+        }
+    std::vector<uint32_t> lf, lb;
+    std::vector<int32_t> of, ob;
+    tiles(Bf, ncf, ncf / BNT, false, 0, 3 * Nk, lf, of);
+    tiles(Bb, nc1, Np / (32 * NH), true, 0, 3 * Qk, lb, ob);
+    auto up = [&](void **dst, const void *src, size_t b) -> bool {
+      if (cudaMalloc(dst, b ? b : 4) != cudaSuccess) return false;
+      return !b || cudaMemcpy(*dst, src, b, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    bool okm = up((void **)&D.Bf, Bf.data(), Bf.size() * 8) && up((void **)&D.Bb, Bb.data(), Bb.size() * 8) &&
+               up((void **)&D.ktlf, lf.data(), lf.size() * 4) && up((void **)&D.ktofff, of.data(), of.size() * 4) &&
+               up((void **)&D.ktlb, lb.data(), lb.size() * 4) && up((void **)&D.ktoffb, ob.data(), ob.size() * 4) &&
+               up((void **)&D.SWe, c->h_swe.data(), c->h_swe.size() * 8) &&
+               up((void **)&D.SWm, c->h_swm.data(), c->h_swm.size() * 8);
+    if (!okm) return dgm::set_err(c, DGM_ENOMEM, "dense_build: material-point operators");
+    D.ncf = ncf;
+    CUDA_TRY(c, cudaMalloc(&D.AC, sizeof(double) * 3 * (size_t)Nk * (size_t)(n_or1(c))));
+    CUDA_TRY(c, cudaMemset(D.AC, 0, sizeof(double) * 3 * (size_t)Nk * (size_t)(n_or1(c))));
+    CUDA_TRY(c, cudaMalloc(&D.P, sizeof(double) * 3 * (size_t)Qk * (size_t)(n_or1(c))));
+  }
   CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NFk * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
   return DGM_OK;
 }
@@ -391,6 +516,10 @@ void free_ctx(dgm_ctx *c) {
     if (c->gev[i]) cudaEventDestroy(c->gev[i]);
   cudaFree(c->d_dense);
   cudaFree(c->dense.AB);
+  for (void *q : {(void *)c->dense.Bf, (void *)c->dense.Bb, (void *)c->dense.ktlf, (void *)c->dense.ktofff,
+                  (void *)c->dense.ktlb, (void *)c->dense.ktoffb, (void *)c->dense.SWe, (void *)c->dense.SWm,
+                  (void *)c->dense.AC, (void *)c->dense.P})
+    cudaFree(q);
   cudaFree(c->d_stream);
   cudaFree(c->d_geo);
   cudaFree(c->d_nbr);
@@ -420,7 +549,7 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   if (order < 1 || order > DGM_PMAX)
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
-  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0};
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0, 0};
   if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_DENSE) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
   if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
     return dgm::set_err(c, DGM_EINVAL, "unknown flux");
@@ -445,6 +574,29 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
     c->mixed = 1;
   }
   c->NH = c->mixed ? p * (p + 1) * (p + 2) / 6 : c->N;
+  // materials at the quadrature points (reverse numerical integration)
+  if (o.material_points) {
+    if (o.flux != DGM_FLUX_CENTRAL) return dgm::set_err(c, DGM_EINVAL, "material_points: central flux only");
+    if (o.mixed_order) return dgm::set_err(c, DGM_EINVAL, "material_points: not with mixed orders");
+    if (o.engine == DGM_ENGINE_SPARSE) return dgm::set_err(c, DGM_EINVAL, "material_points need the dense engine");
+    c->engine = 1;
+    c->matq = 1;
+    std::vector<double> xi, w;
+    tet_quadrature(p, xi, w);
+    const int64_t Q = (int64_t)w.size();
+    c->Q = (int)Q;
+    c->Qk = (int)((Q + 15) / 16 * 16);
+    c->h_swe.assign((size_t)n * c->Qk, 0.0);
+    c->h_swm.assign((size_t)n * c->Qk, 0.0);
+    for (int64_t t = 0; t < n; ++t)
+      for (int64_t i = 0; i < Q; ++i) {
+        const double e = eps[t * Q + i], u = mu[t * Q + i];
+        if (!(e > 0) || !(u > 0) || !std::isfinite(e) || !std::isfinite(u))
+          return dgm::set_err(c, DGM_EINVAL, "tet " + std::to_string(t) + ": point eps/mu must be positive");
+        c->h_swe[(size_t)t * c->Qk + i] = w[i] / e;   // quadrature weight / material
+        c->h_swm[(size_t)t * c->Qk + i] = w[i] / u;
+      }
+  }
   auto rep = [&](int32_t v) -> int64_t { return m->rep ? (int64_t)m->rep[v] : (int64_t)v; };
 
   // ---- validate vertex ids and canonical (ascending-rep) order
@@ -461,8 +613,8 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   // ---- materials
   std::vector<double> ev(n), mv(n);
   for (int64_t t = 0; t < n; ++t) {
-    ev[t] = o.eps_per_elem ? eps[t] : eps[0];
-    mv[t] = o.mu_per_elem ? mu[t] : mu[0];
+    ev[t] = c->matq ? 1.0 : o.eps_per_elem ? eps[t] : eps[0];   // point materials: applied in the inverse mass
+    mv[t] = c->matq ? 1.0 : o.mu_per_elem ? mu[t] : mu[0];
     if (!(ev[t] > 0) || !(mv[t] > 0) || !std::isfinite(ev[t]) || !std::isfinite(mv[t]))
       return dgm::set_err(c, DGM_EINVAL, "tet " + std::to_string(t) + ": eps/mu must be positive");
   }
@@ -968,6 +1120,7 @@ dgm_status dgm_energy_sc(dgm_ctx *c, const double *E, const double *H, const dou
 
 dgm_status dgm_spectral_radius(dgm_ctx *c, int iters, uint64_t seed, double *rho_out, void *stream) {
   if (!c || !rho_out || iters < 1) return dgm::set_err(c, DGM_EINVAL, "bad spectral_radius arguments");
+  if (c->matq) return dgm::set_err(c, DGM_EINVAL, "spectral_radius: not for material_points contexts");
   cudaStream_t st = (cudaStream_t)stream;
   const size_t bytes = sizeof(double) * 3 * (size_t)c->n_tet * c->LD;
   for (int i = 0; i < 3; ++i)
@@ -1012,6 +1165,7 @@ dgm_status dgm_spectral_radius(dgm_ctx *c, int iters, uint64_t seed, double *rho
 
 dgm_status dgm_energy(dgm_ctx *c, const double *E, const double *H, double *out, void *stream) {
   if (!c || !E || !H || !out) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  if (c->matq) return dgm::set_err(c, DGM_EINVAL, "dgm_energy: not for material_points contexts");
   return dgm::launch_energy(c, E, H, out, (cudaStream_t)stream);
 }
 
@@ -1022,6 +1176,16 @@ dgm_status dgm_tables(const dgm_ctx *c, int32_t *nbr, int8_t *nbr_face, int8_t *
   if (nbr_face) std::memcpy(nbr_face, c->nbrf.data(), n);
   if (sign) std::memcpy(sign, c->sign.data(), n);
   if (bc) std::memcpy(bc, c->bc.data(), n);
+  return DGM_OK;
+}
+
+dgm_status dgm_quadrature_host(int order, int64_t *Q, double *xi, double *w) {
+  if (order < 1 || order > DGM_PMAX || !Q) return DGM_EINVAL;
+  std::vector<double> x, ww;
+  tet_quadrature(order, x, ww);
+  *Q = (int64_t)ww.size();
+  if (xi) std::memcpy(xi, x.data(), x.size() * 8);
+  if (w) std::memcpy(w, ww.data(), ww.size() * 8);
   return DGM_OK;
 }
 

@@ -93,6 +93,13 @@ struct DenseOps {
   int32_t *ktoff1[2][4] = {};
   uint32_t *ktl2[2] = {nullptr, nullptr};
   int32_t *ktoff2[2] = {nullptr, nullptr};
+  // material points (reverse numerical integration): Bf [3Nk][ncf] residual -> point
+  // values, Bb [3Qk][nc1] point values -> modes; SWe/SWm [n][Qk] = ŵ_i / ε, μ at the
+  // points; AC [n][3Nk] residual scratch, P [n][3Qk] point-value scratch
+  double *Bf = nullptr, *Bb = nullptr, *SWe = nullptr, *SWm = nullptr, *AC = nullptr, *P = nullptr;
+  uint32_t *ktlf = nullptr, *ktlb = nullptr;
+  int32_t *ktofff = nullptr, *ktoffb = nullptr;
+  int ncf = 0;
 };
 
 struct DevProgs {
@@ -148,6 +155,9 @@ struct dgm_ctx {
   int sms = 0;
   int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
   int mixed = 0;       // 1: H ∈ P^{p-1} (E ∈ P^p), dense engine only; NH = N(p-1)
+  int matq = 0;        // 1: ε, μ given at the quadrature points (dense engine, central flux)
+  int Q = 0, Qk = 0;   // quadrature points per element (collapsed Gauss–Jacobi, q = p+2), padded
+  std::vector<double> h_swe, h_swm;
   int NH = 0;
   dgm::DenseOps dense{};
   void *d_dense = nullptr;
