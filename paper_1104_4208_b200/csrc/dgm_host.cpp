@@ -972,7 +972,10 @@ dgm_status run_steps(dgm_ctx *c, double *E, double *H, double dt, int64_t nsteps
   // serves every chunk).  Small meshes are launch-bound; the graph removes the
   // per-kernel launch cost.  Same kernels, same order: bit-identical results.
   constexpr int64_t kGraphSteps = 32;
-  const bool graphs = c->use_graphs && !h_done && nsteps >= 2 * kGraphSteps && r == DGM_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);   // the caller may be capturing us into its own graph
+  const bool graphs = c->use_graphs && !h_done && nsteps >= 2 * kGraphSteps && r == DGM_OK &&
+                      cap == cudaStreamCaptureStatusNone;
   if (graphs) {
     const GraphKey key{E, H, HF, dt, ce, ch};
     if (!c->gexec || !(c->gkey == key)) {

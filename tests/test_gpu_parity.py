@@ -333,3 +333,29 @@ def test_graph_replay_matches_single_steps(case, p, engine):
         for _ in range(99):
             c.dgm_step_ex(E2, H2, dt, 1, DGM_STEP_CONTINUE)
         assert bool((E1 == E2).all()) and bool((H1 == H2).all())
+
+
+def test_step_capturable_into_user_graph():
+    """A caller can capture dgm_step (even a long one, which would otherwise use the
+    library's own graph) into its own CUDA graph; replaying it equals direct calls."""
+    import torch
+    m, rep, eps, mu = _problem(2, (False,) * 3, 3, "central")
+    c = _ctx(m, rep, 3, eps, mu, "central")
+    rng = np.random.default_rng(3)
+    E = rng.standard_normal((3, m.n_tet, c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N))
+    E1, H1 = c.to_device(E), c.to_device(H)
+    c.dgm_step(E1, H1, 1e-3, 70)
+    E2, H2 = c.to_device(E), c.to_device(H)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        c.dgm_step(E2, H2, 1e-3, 1, stream=s)   # entry traces outside the capture
+        torch.cuda.synchronize()
+    E2.copy_(c.to_device(E))
+    H2.copy_(c.to_device(H))
+    with torch.cuda.graph(g, stream=s):
+        c.dgm_step(E2, H2, 1e-3, 70, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert bool((E1 == E2).all()) and bool((H1 == H2).all())
