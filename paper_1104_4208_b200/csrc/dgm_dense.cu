@@ -32,22 +32,20 @@ namespace {
 
 constexpr int BN = 96, BK = 16;  // BN: one warp column = three 32-column blocks
 constexpr int WM = 16;             // warp tile: 16 rows x 96 columns (2 x 12 MMAs of 8x8)
-constexpr int NH = kDenseNH;       // warp columns per CTA: CTA tile = BM x (96 NH)
-constexpr int BNT = BN * NH;
-constexpr int BST = BNT + 4;       // padded smem strides (conflict-free fragment loads)
 constexpr int AKS = BK + 4;        // A tile row stride ([m][k] layout)
 
 // CTA shape: BM elements x BNT columns; (BM/16) x NH warps.  Warps of one warp column
 // see the same operator block mask.
-template <int BM_, int NST_>
+template <int BM_, int NST_, int NH_>
 struct Cfg {
-  static constexpr int BM = BM_, NSTAGE = NST_, NTHREADS = (BM_ / WM) * NH * 32;
-  static constexpr int MINB = NH == 1 ? (BM_ == 32 ? 4 : (BM_ == 64 ? 3 : 1)) : (BM_ == 64 ? 2 : 1);
+  static constexpr int NH = NH_, BNT = BN * NH_, BST = BN * NH_ + 4;   // padded (conflict-free fragment loads)
+  static constexpr int BM = BM_, NSTAGE = NST_, NTHREADS = (BM_ / WM) * NH_ * 32;
+  static constexpr int MINB = NH_ == 1 ? (BM_ == 32 ? 4 : (BM_ == 64 ? 3 : 1)) : (BM_ == 64 ? 2 : 1);
   struct Smem {
     double A[NST_][BM_][AKS];
-    double B[NST_][BK][BST];
+    double B[NST_][BK][BN * NH_ + 4];
   };
-  static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * BST + BM_ * 8);   // C tile + geometry rows
+  static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * (BN * NH_ + 4) + BM_ * 8);   // C tile + geometry
   static constexpr size_t SMEM = sizeof(Smem) > EPI_BYTES ? sizeof(Smem) : EPI_BYTES;
 };
 
@@ -112,7 +110,7 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 template <int EPI, class C>
 __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, int st, int64_t m0, int nt, int kt,
                                           int tid) {
-  constexpr int BM = C::BM, NTHREADS = C::NTHREADS;
+  constexpr int BM = C::BM, NTHREADS = C::NTHREADS, NH = C::NH, BNT = C::BNT;
   const int k0 = kt * BK;
   const bool lo = k0 < g.k1;
   int blk, q0, lim;   // block index, first in-block index of the tile, valid count in the block
@@ -152,7 +150,7 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
 
 template <int EPI, class C>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) {
-  constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS;
+  constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS, NH = C::NH, BNT = C::BNT, BST = C::BST;
   extern __shared__ __align__(16) unsigned char dsm[];
   typename C::Smem &sm = *reinterpret_cast<typename C::Smem *>(dsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -187,7 +185,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
-      if (s < nk) load_tile<EPI, C>(g, sm, s, m0, nt, (int)(kts[s] & 0xFFFFu), tid);
+      if (s < nk) load_tile<EPI, C>(g, sm, s, m0, nt, (int)(kts[s] & 0xFFu), tid);
       cp_commit();
     }
     uint32_t kcur = nk > 0 ? kts[0] : 0u;
@@ -196,7 +194,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       cp_wait<NSTAGE - 2>();
       __syncthreads();
       const int nx = it + NSTAGE - 1;
-      if (nx < nk) load_tile<EPI, C>(g, sm, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFFFu), tid);
+      if (nx < nk) load_tile<EPI, C>(g, sm, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFu), tid);
       cp_commit();
       const int st = it % NSTAGE;
       double a[BK / 4][2];
@@ -204,7 +202,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
-      const unsigned m12 = (kcur >> 16) & 0xFFFu;   // non-zero 16x8 column groups of this k-tile
+      const unsigned m12 = (kcur >> (8 + 12 * wn)) & 0xFFFu;   // this warp column's non-zero 16x8 groups
       kcur = knext;
       // skip zero operator blocks: a CTA-uniform branch per 32-column block, then per
       // 8-column group (whole 16-row k-tile each, so the tensor pipe is not occupied)
@@ -414,14 +412,22 @@ int dense_cfg() {
   return v && *v ? std::atoi(v) : 0;
 }
 
+template <int EPI, int NHV>
+dgm_status gemm_go_nh(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
+  switch (dense_cfg()) {
+    case 1: return gemm_go_c<EPI, Cfg<64, 4, NHV>>(c, g, st);
+    case 2: return gemm_go_c<EPI, Cfg<128, 3, NHV>>(c, g, st);
+    case 3: return gemm_go_c<EPI, Cfg<32, 4, NHV>>(c, g, st);
+    default: return gemm_go_c<EPI, Cfg<64, 3, NHV>>(c, g, st);
+  }
+}
+
+// stage GEMMs: one warp column (gathered component blocks); trace-type GEMMs: the
+// context's choice (two warp columns halve the A re-reads at p >= 8)
 template <int EPI>
 dgm_status gemm_go(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
-  switch (dense_cfg()) {
-    case 1: return gemm_go_c<EPI, Cfg<64, 4>>(c, g, st);
-    case 2: return gemm_go_c<EPI, Cfg<128, 3>>(c, g, st);
-    case 3: return gemm_go_c<EPI, Cfg<32, 4>>(c, g, st);
-    default: return gemm_go_c<EPI, Cfg<64, 3>>(c, g, st);
-  }
+  if (EPI == EPI_TRACE && c->dense.trace_nh == 2) return gemm_go_nh<EPI, 2>(c, g, st);
+  return gemm_go_nh<EPI, 1>(c, g, st);
 }
 
 }  // namespace
@@ -457,7 +463,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
   g.ktl = D.ktl1[v][sel];
   g.ktoff = D.ktoff1[v][sel];
-  g.ntiles_n = D.nc1 / 3 / (32 * NH);
+  g.ntiles_n = D.nc1 / 3 / (32 * kDenseNH1);
   g.n_tet = c->n_tet;
   g.N = c->N;
   g.NF = c->NF;
@@ -492,7 +498,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     f.NC = D.ncf;
     f.ktl = D.ktlf;
     f.ktoff = D.ktofff;
-    f.ntiles_n = D.ncf / BNT;
+    f.ntiles_n = D.ncf / (BN * D.trace_nh);
     f.n_tet = c->n_tet;
     f.ncols = 3 * Qk;
     f.tr = D.P;
@@ -536,7 +542,7 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
   g.NC = D.nc2;
   g.ktl = D.ktl2[field];
   g.ktoff = D.ktoff2[field];
-  g.ntiles_n = D.nc2 / BNT;
+  g.ntiles_n = D.nc2 / (BN * D.trace_nh);
   g.n_tet = c->n_tet;
   g.N = c->N;
   g.NF = c->NF;

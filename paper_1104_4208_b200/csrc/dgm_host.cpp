@@ -305,13 +305,15 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   static const double T1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
   static const double T2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
   const int N = c->N, NF = c->NF;
-  constexpr int NH = dgm::kDenseNH, BNT = BN * NH;
+  constexpr int NH = dgm::kDenseNH1, BNT = BN * NH;
+  c->dense.trace_nh = c->p >= 8 ? 2 : 1;   // measured: wider trace tiles win from p = 8
+  const int BNT2 = BN * c->dense.trace_nh;
   const int Nk = (N + BK - 1) / BK * BK, NFk = (NF + BK - 1) / BK * BK, Np = (N + 32 * NH - 1) / (32 * NH) * (32 * NH);
   const int k1a = 3 * Nk;
   const int K1 = k1a + 8 * NFk;
   const int K2 = 3 * Nk;
   const int nc1 = 3 * Np;
-  const int nc2 = (8 * NF + BNT - 1) / BNT * BNT;
+  const int nc2 = (8 * NF + BNT2 - 1) / BNT2 * BNT2;
   std::vector<double> B1((size_t)K1 * nc1, 0.0), B2((size_t)K2 * nc2, 0.0);
   // curl: column (c, β) of Ĉ by running the sweep program on that unit input
   int maxslot = 0;
@@ -366,24 +368,26 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   // per n-tile: non-zero k-tiles with the mask of non-zero 16x8 column groups
   constexpr int GW = 8;   // 16x8 blocks (one MMA column group); 12 mask bits per k-tile
   auto tiles = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int klo, int khi,
-                   std::vector<uint32_t> &ktl, std::vector<int32_t> &ktoff) {
+                   std::vector<uint32_t> &ktl, std::vector<int32_t> &ktoff, int bnt_arg = 0) {
     ktl.clear();
     ktoff.assign(1, 0);
+    const int bnt = bnt_arg > 0 ? bnt_arg : BNT;
+    const int nh = bnt / BN;
     for (int t = 0; t < ntn; ++t) {
       for (int kt = klo / BK; kt < khi / BK; ++kt) {
-        uint32_t mask = 0;
-        for (int grp = 0; grp < BNT / GW; ++grp)
+        uint32_t mask = 0;   // 12 bits per warp column: its non-zero 16x8 groups
+        for (int grp = 0; grp < bnt / GW; ++grp)
           for (int cc = 0; cc < GW && !(mask >> grp & 1); ++cc) {
             const int tc = grp * GW + cc;   // column within the CTA tile; warp column h = tc / 96
             const int h = tc / BN, t3 = tc % BN;
-            const int col = gather ? (t3 / 32) * Np + 32 * (NH * t + h) + t3 % 32 : t * BNT + tc;
+            const int col = gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + tc;
             for (int k = kt * BK; k < (kt + 1) * BK; ++k)
               if (B[(size_t)k * nc + col] != 0.0) {
                 mask |= 1u << grp;
                 break;
               }
           }
-        if (mask) ktl.push_back((uint32_t)kt | (mask << 16));
+        if (mask) ktl.push_back((uint32_t)kt | (mask << 8));   // kt < 256: K <= 4096 rows
       }
       ktoff.push_back((int32_t)ktl.size());
     }
@@ -415,12 +419,12 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     tiles(B1v[v], nc1, Np / (32 * NH), true, 0, k1a, l1[v][1], o1[v][1]);
     tiles(B1v[v], nc1, Np / (32 * NH), true, k1a, K1, l1[v][2], o1[v][2]);
     tiles(B1v[v], nc1, Np / (32 * NH), true, 0, K1, l1[v][3], o1[v][3]);
-    tiles(B2v[v], nc2, nc2 / BNT, false, 0, K2, l2[v], o2[v]);
+    tiles(B2v[v], nc2, nc2 / BNT2, false, 0, K2, l2[v], o2[v], BNT2);
   }
   if (std::getenv("DGM_DEBUG_DENSE")) {
     auto bits = [](const std::vector<uint32_t> &l) {
       long n = 0;
-      for (uint32_t x : l) n += __builtin_popcount(x >> 16);
+      for (uint32_t x : l) n += __builtin_popcount(x >> 8);
       return n;
     };
     std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x32)\n", c->p,
@@ -477,7 +481,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     tet_quadrature(c->p, xi, w);
     std::vector<double> Phi((size_t)Q * N);
     for (int i = 0; i < Q; ++i) basis_at(c->p, &xi[3 * i], &Phi[(size_t)i * N]);
-    const int ncf = (3 * Qk + BNT - 1) / BNT * BNT;
+    const int ncf = (3 * Qk + BNT2 - 1) / BNT2 * BNT2;
     std::vector<double> Bf((size_t)3 * Nk * ncf, 0.0), Bb((size_t)3 * Qk * nc1, 0.0);
     for (int cc = 0; cc < 3; ++cc)
       for (int b = 0; b < N; ++b)
@@ -487,7 +491,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
         }
     std::vector<uint32_t> lf, lb;
     std::vector<int32_t> of, ob;
-    tiles(Bf, ncf, ncf / BNT, false, 0, 3 * Nk, lf, of);
+    tiles(Bf, ncf, ncf / BNT2, false, 0, 3 * Nk, lf, of, BNT2);
     tiles(Bb, nc1, Np / (32 * NH), true, 0, 3 * Qk, lb, ob);
     auto up = [&](void **dst, const void *src, size_t b) -> bool {
       if (cudaMalloc(dst, b ? b : 4) != cudaSuccess) return false;
