@@ -59,8 +59,13 @@ struct GemmArgs {
   const double *p0, *p1;
   int64_t ld0, ld1, cs;
   int k1, Nk, NFk;
-  // B operand: [Kpad][NC] row-major; per n-tile the list of non-zero k-tiles
+  // k-tile geometry: k-tiles per A block below / above k1 (and float reciprocals)
+  int k1t, nkA, nkF;
+  float rnkA, rnkF;
+  // B operand: pre-tiled pool [ntiles_n][nkt][BK][BST] (host: dense_build tile_pool);
+  // per n-tile the list of non-zero k-tiles
   const double *Bm;
+  int nkt;
   int NC;
   int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t, warp column h gathers
                            // β in [32(NH t + h), +32)
@@ -106,45 +111,41 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// load k-tile kt of A ([m][k], 16-byte copies of mode pairs) and B into stage st
+// load k-tile kt of A ([m][k], 16-byte copies of mode pairs) and B into stage st.
+// Thread tid copies A rows mA + i NTHREADS/8 at mode pair kp (the same pair for every
+// row), so per k-tile only the block base and the zero-fill bound are recomputed.
+// B comes from the pre-tiled pool (one [BK][BST] tile per (n-tile, k-tile), already
+// in the shared-memory layout): a linear copy.
 template <int EPI, class C>
 __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, int st, int64_t m0, int nt, int kt,
                                           int tid) {
-  constexpr int BM = C::BM, NTHREADS = C::NTHREADS, NH = C::NH, BNT = C::BNT;
-  const int k0 = kt * BK;
-  const bool lo = k0 < g.k1;
-  int blk, q0, lim;   // block index, first in-block index of the tile, valid count in the block
-  if (lo) {
-    blk = k0 / g.Nk;
-    q0 = k0 - blk * g.Nk;
-    lim = g.Na;
-  } else {
-    blk = (k0 - g.k1) / g.NFk;
-    q0 = (k0 - g.k1) - blk * g.NFk;
-    lim = g.NF;
-  }
-  const double *base = lo ? g.p0 + blk * g.cs : g.p1 + (int64_t)blk * g.NFk;
+  constexpr int BM = C::BM, NTHREADS = C::NTHREADS, BST = C::BST;
+  constexpr int RSTEP = NTHREADS / 8;   // rows between one thread's A copies
+  const bool lo = kt < g.k1t;
+  // block index and first in-block row of the tile: small exact quotients by float
+  // reciprocal ((kt + 0.5)/n is at least 0.5/n away from an integer)
+  const int kr = lo ? kt : kt - g.k1t;
+  const int blk = (int)(((float)kr + 0.5f) * (lo ? g.rnkA : g.rnkF));
+  const int q0 = (kr - blk * (lo ? g.nkA : g.nkF)) * BK;
+  const int lim = lo ? g.Na : g.NF;
   const int64_t ld = lo ? g.ld0 : g.ld1;
+  const int mA = tid >> 3, kp = tid & 7;
+  const int q = q0 + 2 * kp;
+  const int bq = q + 1 < lim ? 16 : (q < lim ? 8 : 0);
+  const double *src = (lo ? g.p0 + blk * g.cs : g.p1 + (int64_t)blk * g.NFk) + (m0 + mA) * ld + q;
+  const int64_t e0 = m0 + mA;
 #pragma unroll
-  for (int i = 0; i < BM * (BK / 2) / NTHREADS; ++i) {
-    const int idx = tid + i * NTHREADS;
-    const int m = idx >> 3, kp = idx & 7;
-    const int64_t e = m0 + m;
-    const int q = q0 + 2 * kp;
-    int bytes = q + 1 < lim ? 16 : (q < lim ? 8 : 0);
-    if (e >= g.n_tet) bytes = 0;
-    cpa16z(&sm.A[st][m][2 * kp], bytes ? base + e * ld + q : g.p0, bytes);
+  for (int i = 0; i < BM / RSTEP; ++i) {
+    const int bytes = e0 + i * RSTEP < g.n_tet ? bq : 0;
+    cpa16z(&sm.A[st][mA + i * RSTEP][2 * kp], bytes ? src + i * RSTEP * ld : g.p0, bytes);
   }
-  const double *bsrc = g.Bm + (int64_t)kt * BK * g.NC;
+  constexpr int NCP = BK * BST / 2;   // 16-byte copies per B tile
+  const double *bsrc = g.Bm + ((int64_t)nt * g.nkt + kt) * (BK * BST);
+  double *bdst = &sm.B[st][0][0];
 #pragma unroll
-  for (int i = 0; i < BK * BNT / 2 / NTHREADS; ++i) {
+  for (int i = 0; i < (NCP + NTHREADS - 1) / NTHREADS; ++i) {
     const int idx = tid + i * NTHREADS;
-    const int r = idx / (BNT / 2), c2 = idx - r * (BNT / 2);
-    // EPI_STAGE: warp column h = c2 / 48 gathers the three component blocks of modes
-    // [32(NH nt + h), +32); traces are contiguous
-    const int h = c2 / (BN / 2), c3 = c2 - h * (BN / 2);
-    const int col = EPI == EPI_STAGE ? (c3 >> 4) * g.Np + 32 * (NH * nt + h) + 2 * (c3 & 15) : nt * BNT + 2 * c2;
-    cpa16(&sm.B[st][r][2 * c2], bsrc + (int64_t)r * g.NC + col);
+    if (NCP % NTHREADS == 0 || idx < NCP) cpa16(bdst + 2 * idx, bsrc + 2 * idx);
   }
 }
 
@@ -391,7 +392,13 @@ __global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, d
 }
 
 template <int EPI, class C>
-dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
+dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g0, cudaStream_t st) {
+  GemmArgs g = g0;
+  g.k1t = g.k1 / BK;
+  g.nkA = g.Nk / BK;
+  g.nkF = g.NFk / BK;
+  g.rnkA = 1.0f / (float)g.nkA;
+  g.rnkF = 1.0f / (float)g.nkF;
   const size_t smem = C::SMEM;
   auto kern = gemm_kernel<EPI, C>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -457,6 +464,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.Nk = D.k1a / 3;
   g.NFk = (c->NF + BK - 1) / BK * BK;
   g.Bm = D.B1[v];
+  g.nkt = D.nkt1;
   g.NC = D.nc1;
   g.Np = D.nc1 / 3;
   // curl only / flux only: restrict the k-tile lists
@@ -495,6 +503,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     f.NFk = Nk;
     f.Na = c->N;
     f.Bm = D.Bf;
+    f.nkt = D.nktf;
     f.NC = D.ncf;
     f.ktl = D.ktlf;
     f.ktoff = D.ktofff;
@@ -515,6 +524,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     b.NFk = Qk;
     b.Na = c->Q;
     b.Bm = D.Bb;
+    b.nkt = D.nktb;
     b.ktl = D.ktlb;
     b.ktoff = D.ktoffb;
     b.unit_m = 1;
@@ -539,6 +549,7 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
   g.NFk = (c->NF + BK - 1) / BK * BK;
   g.Na = c->N;
   g.Bm = D.B2[field];
+  g.nkt = D.nkt2;
   g.NC = D.nc2;
   g.ktl = D.ktl2[field];
   g.ktoff = D.ktoff2[field];

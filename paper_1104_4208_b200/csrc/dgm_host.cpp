@@ -392,6 +392,22 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
       ktoff.push_back((int32_t)ktl.size());
     }
   };
+  // pre-tiled operator pool [n-tile][k-tile][BK][bnt + 4]: every (n-tile, k-tile) tile
+  // in the GEMM's shared-memory layout (same column gather as `tiles`), so a k-tile
+  // load is one linear copy
+  auto pool = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int bnt) {
+    const int nh = bnt / BN, bst = bnt + 4, nkt = (int)(B.size() / nc) / BK;
+    std::vector<double> P((size_t)ntn * nkt * BK * bst, 0.0);
+    for (int t = 0; t < ntn; ++t)
+      for (int kt = 0; kt < nkt; ++kt)
+        for (int r = 0; r < BK; ++r)
+          for (int tc = 0; tc < bnt; ++tc) {
+            const int h = tc / BN, t3 = tc % BN;
+            const int col = gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + tc;
+            P[(((size_t)t * nkt + kt) * BK + r) * bst + tc] = B[(size_t)(kt * BK + r) * nc + col];
+          }
+    return P;
+  };
   // variants per updated field (0: E, 1: H); mixed orders (H ∈ P^{p-1}, NH = N(p-1)):
   // the E stage ignores H's modes >= NH as curl input, the H stage has no outputs
   // there, and H's traces ignore them (face modes > p of the lift/trace vanish exactly
@@ -430,11 +446,16 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x32)\n", c->p,
                  l1[0][3].size(), bits(l1[0][3]), l2[0].size(), bits(l2[0]));
   }
+  std::vector<double> P1[2], P2[2];
+  for (int v = 0; v < nvar; ++v) {
+    P1[v] = pool(B1v[v], nc1, Np / (32 * NH), true, BNT);
+    P2[v] = pool(B2v[v], nc2, nc2 / BNT2, false, BNT2);
+  }
   // one device allocation
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   size_t bytes = 0;
   for (int v = 0; v < nvar; ++v) {
-    bytes += al(B1.size() * 8) + al(B2.size() * 8) + al(l2[v].size() * 4 + 4) + al(o2[v].size() * 4);
+    bytes += al(P1[v].size() * 8) + al(P2[v].size() * 8) + al(l2[v].size() * 4 + 4) + al(o2[v].size() * 4);
     for (int i = 1; i < 4; ++i) bytes += al(l1[v][i].size() * 4 + 4) + al(o1[v][i].size() * 4);
   }
   CUDA_TRY(c, cudaMalloc(&c->d_dense, bytes));
@@ -449,8 +470,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   };
   dgm::DenseOps &D = c->dense;
   for (int v = 0; v < nvar; ++v) {
-    D.B1[v] = (double *)put(B1v[v].data(), B1v[v].size() * 8);
-    D.B2[v] = (double *)put(B2v[v].data(), B2v[v].size() * 8);
+    D.B1[v] = (double *)put(P1[v].data(), P1[v].size() * 8);
+    D.B2[v] = (double *)put(P2[v].data(), P2[v].size() * 8);
     for (int i = 1; i < 4; ++i) {
       D.ktl1[v][i] = (uint32_t *)put(l1[v][i].data(), l1[v][i].size() * 4);
       D.ktoff1[v][i] = (int32_t *)put(o1[v][i].data(), o1[v][i].size() * 4);
@@ -472,6 +493,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   D.nc1 = nc1;
   D.nc2 = nc2;
   D.k1a = k1a;
+  D.nkt1 = K1 / BK;
+  D.nkt2 = K2 / BK;
   if (c->matq) {
     // reverse numerical integration: residual (component-blocked, Nk rows) -> point
     // values (Qk per component) -> weighted by ŵ_i/m(x_i) -> back to modes with
@@ -497,7 +520,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
       if (cudaMalloc(dst, b ? b : 4) != cudaSuccess) return false;
       return !b || cudaMemcpy(*dst, src, b, cudaMemcpyHostToDevice) == cudaSuccess;
     };
-    bool okm = up((void **)&D.Bf, Bf.data(), Bf.size() * 8) && up((void **)&D.Bb, Bb.data(), Bb.size() * 8) &&
+    const std::vector<double> Pf = pool(Bf, ncf, ncf / BNT2, false, BNT2), Pb = pool(Bb, nc1, Np / (32 * NH), true, BNT);
+    D.nktf = 3 * Nk / BK;
+    D.nktb = 3 * Qk / BK;
+    bool okm = up((void **)&D.Bf, Pf.data(), Pf.size() * 8) && up((void **)&D.Bb, Pb.data(), Pb.size() * 8) &&
                up((void **)&D.ktlf, lf.data(), lf.size() * 4) && up((void **)&D.ktofff, of.data(), of.size() * 4) &&
                up((void **)&D.ktlb, lb.data(), lb.size() * 4) && up((void **)&D.ktoffb, ob.data(), ob.size() * 4) &&
                up((void **)&D.SWe, c->h_swe.data(), c->h_swe.size() * 8) &&

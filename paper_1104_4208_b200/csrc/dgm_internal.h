@@ -87,9 +87,13 @@ constexpr int kDenseNH1 = 1;
 // Per updated field v (0: E stage / E traces, 1: H stage / H traces) a variant of the
 // matrices; they differ only for mixed orders (H ∈ P^{p-1}: B1[0] ignores H's modes
 // >= N(p-1) as curl input, B1[1] has no output columns there, B2[1] no rows there).
+// Operators B1, B2, Bf, Bb are stored pre-tiled: [n-tile][k-tile][16][BST], BST =
+// 96 NH + 4, each tile in the GEMM's shared-memory layout (stage type: the three
+// gathered component blocks).
 struct DenseOps {
   double *B1[2] = {nullptr, nullptr}, *B2[2] = {nullptr, nullptr}, *AB = nullptr;
   int nc1 = 0, nc2 = 0, k1a = 0;
+  int nkt1 = 0, nkt2 = 0, nktf = 0, nktb = 0;   // k-tiles of B1, B2, Bf, Bb (pool strides)
   int trace_nh = 1;   // warp columns of the trace-type GEMMs (B2, Bf): 2 for p >= 8
   uint32_t *ktl1[2][4] = {};
   int32_t *ktoff1[2][4] = {};
