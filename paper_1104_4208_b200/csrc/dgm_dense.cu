@@ -46,7 +46,8 @@ struct Cfg {
     double B[NST_][BK][BN * NH_ + 4];
   };
   static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * (BN * NH_ + 4) + BM_ * 8);   // C tile + geometry
-  static constexpr size_t SMEM = sizeof(Smem) > EPI_BYTES ? sizeof(Smem) : EPI_BYTES;
+  static constexpr size_t SMEM_DATA = sizeof(Smem) > EPI_BYTES ? sizeof(Smem) : EPI_BYTES;
+  static constexpr size_t SMEM = SMEM_DATA + 8 * NST_;   // + one mbarrier per stage (B tile)
 };
 
 enum { EPI_STAGE = 0, EPI_TRACE = 1 };
@@ -105,6 +106,30 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NW) : "memory");
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t *m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "MBW_LOOP:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra MBW_DONE;\n\t"
+      "bra MBW_LOOP;\n\t"
+      "MBW_DONE:\n\t}\n" ::"r"(su32(m)),
+      "r"(parity)
+      : "memory");
+}
+// one bulk copy global -> shared (the B tile), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *m) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(m))
+               : "memory");
+}
+
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -115,10 +140,10 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 // Thread tid copies A rows mA + i NTHREADS/8 at mode pair kp (the same pair for every
 // row), so per k-tile only the block base and the zero-fill bound are recomputed.
 // B comes from the pre-tiled pool (one [BK][BST] tile per (n-tile, k-tile), already
-// in the shared-memory layout): a linear copy.
+// in the shared-memory layout): one bulk copy by thread 0 on the stage's mbarrier.
 template <int EPI, class C>
-__device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, int st, int64_t m0, int nt, int kt,
-                                          int tid) {
+__device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, uint64_t *mbar, int st, int64_t m0,
+                                          int nt, int kt, int tid) {
   constexpr int BM = C::BM, NTHREADS = C::NTHREADS, BST = C::BST;
   constexpr int RSTEP = NTHREADS / 8;   // rows between one thread's A copies
   const bool lo = kt < g.k1t;
@@ -139,14 +164,8 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
     const int bytes = e0 + i * RSTEP < g.n_tet ? bq : 0;
     cpa16z(&sm.A[st][mA + i * RSTEP][2 * kp], bytes ? src + i * RSTEP * ld : g.p0, bytes);
   }
-  constexpr int NCP = BK * BST / 2;   // 16-byte copies per B tile
-  const double *bsrc = g.Bm + ((int64_t)nt * g.nkt + kt) * (BK * BST);
-  double *bdst = &sm.B[st][0][0];
-#pragma unroll
-  for (int i = 0; i < (NCP + NTHREADS - 1) / NTHREADS; ++i) {
-    const int idx = tid + i * NTHREADS;
-    if (NCP % NTHREADS == 0 || idx < NCP) cpa16(bdst + 2 * idx, bsrc + 2 * idx);
-  }
+  if (tid == 0)
+    bulk_load(&sm.B[st][0][0], g.Bm + ((int64_t)nt * g.nkt + kt) * (BK * BST), BK * BST * sizeof(double), &mbar[st]);
 }
 
 template <int EPI, class C>
@@ -154,7 +173,15 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
   constexpr int BM = C::BM, NSTAGE = C::NSTAGE, NTHREADS = C::NTHREADS, NH = C::NH, BNT = C::BNT, BST = C::BST;
   extern __shared__ __align__(16) unsigned char dsm[];
   typename C::Smem &sm = *reinterpret_cast<typename C::Smem *>(dsm);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(dsm + C::SMEM_DATA);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(&mbar[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph = 0;   // bit s: parity of the next completion of stage s's B tile
   const int wm = warp % (BM / WM), wn = warp / (BM / WM);
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
   const int64_t mtiles = (g.n_tet + BM - 1) / BM;
@@ -186,18 +213,20 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
-      if (s < nk) load_tile<EPI, C>(g, sm, s, m0, nt, (int)(kts[s] & 0xFFu), tid);
+      if (s < nk) load_tile<EPI, C>(g, sm, mbar, s, m0, nt, (int)(kts[s] & 0xFFu), tid);
       cp_commit();
     }
     uint32_t kcur = nk > 0 ? kts[0] : 0u;
     for (int it = 0; it < nk; ++it) {
       const uint32_t knext = it + 1 < nk ? kts[it + 1] : 0u;   // one ahead: off the critical path
+      const int st = it % NSTAGE;
       cp_wait<NSTAGE - 2>();
+      mbar_wait(&mbar[st], (ph >> st) & 1u);
+      ph ^= 1u << st;
       __syncthreads();
       const int nx = it + NSTAGE - 1;
-      if (nx < nk) load_tile<EPI, C>(g, sm, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFu), tid);
+      if (nx < nk) load_tile<EPI, C>(g, sm, mbar, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFu), tid);
       cp_commit();
-      const int st = it % NSTAGE;
       double a[BK / 4][2];
 #pragma unroll
       for (int k4 = 0; k4 < BK / 4; ++k4)
@@ -317,6 +346,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         }
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // epilogue writes before the next bulk copies
     __syncthreads();
   }
 }
