@@ -137,12 +137,19 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 }
 
 // load k-tile kt of A ([m][k], 16-byte copies of mode pairs) and B into stage st.
-// Thread tid copies A rows mA + i NTHREADS/8 at mode pair kp (the same pair for every
-// row), so per k-tile only the block base and the zero-fill bound are recomputed.
+// Thread tid copies A rows tid/8 + i NTHREADS/8 at mode pair tid%8 (the same pair for
+// every row), so per k-tile only the block base and the zero-fill bound are recomputed.
 // B comes from the pre-tiled pool (one [BK][BST] tile per (n-tile, k-tile), already
 // in the shared-memory layout): one bulk copy by thread 0 on the stage's mbarrier.
+// per-tile part of a thread's A addressing: row offsets of its first row in both
+// A blocks, and how many of its rows exist (ragged last tile)
+struct ARow {
+  int64_t off0, off1;
+  int nrow;
+};
+
 template <int EPI, class C>
-__device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, uint64_t *mbar, int st, int64_t m0,
+__device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &sm, uint64_t *mbar, int st, const ARow &ar,
                                           int nt, int kt, int tid) {
   constexpr int BM = C::BM, NTHREADS = C::NTHREADS, BST = C::BST;
   constexpr int RSTEP = NTHREADS / 8;   // rows between one thread's A copies
@@ -153,16 +160,17 @@ __device__ __forceinline__ void load_tile(const GemmArgs &g, typename C::Smem &s
   const int blk = (int)(((float)kr + 0.5f) * (lo ? g.rnkA : g.rnkF));
   const int q0 = (kr - blk * (lo ? g.nkA : g.nkF)) * BK;
   const int lim = lo ? g.Na : g.NF;
-  const int64_t ld = lo ? g.ld0 : g.ld1;
-  const int mA = tid >> 3, kp = tid & 7;
+  const int kp = tid & 7;
   const int q = q0 + 2 * kp;
   const int bq = q + 1 < lim ? 16 : (q < lim ? 8 : 0);
-  const double *src = (lo ? g.p0 + blk * g.cs : g.p1 + (int64_t)blk * g.NFk) + (m0 + mA) * ld + q;
-  const int64_t e0 = m0 + mA;
+  const double *src = lo ? g.p0 + blk * g.cs + ar.off0 + q : g.p1 + (int64_t)blk * g.NFk + ar.off1 + q;
+  const int64_t rs = RSTEP * (lo ? g.ld0 : g.ld1);
+  double *dst = &sm.A[st][tid >> 3][2 * kp];
 #pragma unroll
   for (int i = 0; i < BM / RSTEP; ++i) {
-    const int bytes = e0 + i * RSTEP < g.n_tet ? bq : 0;
-    cpa16z(&sm.A[st][mA + i * RSTEP][2 * kp], bytes ? src + i * RSTEP * ld : g.p0, bytes);
+    // zero-size copies read nothing (zero fill), so the pointer of a missing row is not used
+    cpa16z(dst + i * RSTEP * AKS, src, i * RSTEP < ar.nrow ? bq : 0);
+    src += rs;
   }
   if (tid == 0)
     bulk_load(&sm.B[st][0][0], g.Bm + ((int64_t)nt * g.nkt + kt) * (BK * BST), BK * BST * sizeof(double), &mbar[st]);
@@ -210,10 +218,18 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         }
       }
     }
+    ARow ar;
+    {
+      const int64_t eA = m0 + (tid >> 3);
+      ar.off0 = eA * g.ld0;
+      ar.off1 = eA * g.ld1;
+      const int64_t nr = g.n_tet - eA;
+      ar.nrow = nr > BM ? BM : (int)nr;
+    }
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
-      if (s < nk) load_tile<EPI, C>(g, sm, mbar, s, m0, nt, (int)(kts[s] & 0xFFu), tid);
+      if (s < nk) load_tile<EPI, C>(g, sm, mbar, s, ar, nt, (int)(kts[s] & 0xFFu), tid);
       cp_commit();
     }
     uint32_t kcur = nk > 0 ? kts[0] : 0u;
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       ph ^= 1u << st;
       __syncthreads();
       const int nx = it + NSTAGE - 1;
-      if (nx < nk) load_tile<EPI, C>(g, sm, mbar, nx % NSTAGE, m0, nt, (int)(kts[nx] & 0xFFu), tid);
+      if (nx < nk) load_tile<EPI, C>(g, sm, mbar, nx % NSTAGE, ar, nt, (int)(kts[nx] & 0xFFu), tid);
       cp_commit();
       double a[BK / 4][2];
 #pragma unroll
