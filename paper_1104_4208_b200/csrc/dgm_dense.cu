@@ -136,6 +136,23 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// NJ consecutive 8-column groups j0.. of one k-tile: k4 outermost, so the 2 NJ
+// DMMAs of one k4 step are independent (hides the DMMA dependency latency)
+template <int NJ, int BST>
+__device__ __forceinline__ void mma_cols(double (&acc)[12][2][2], const double (&a)[BK / 4][2], const double *bw,
+                                         int j0) {
+#pragma unroll
+  for (int k4 = 0; k4 < BK / 4; ++k4) {
+    double b[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) b[j] = bw[k4 * 4 * BST + (j0 + j) * 8];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) dmma(acc[j0 + j][i][0], acc[j0 + j][i][1], a[k4][i], b[j]);
+  }
+}
+
 // load k-tile kt of A ([m][k], 16-byte copies of mode pairs) and B into stage st.
 // Thread tid copies A rows tid/8 + i NTHREADS/8 at mode pair tid%8 (the same pair for
 // every row), so per k-tile only the block base and the zero-fill bound are recomputed.
@@ -250,20 +267,26 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
       const unsigned m12 = (kcur >> (8 + 12 * wn)) & 0xFFFu;   // this warp column's non-zero 16x8 groups
       kcur = knext;
-      // skip zero operator blocks: a CTA-uniform branch per 32-column block, then per
-      // 8-column group (whole 16-row k-tile each, so the tensor pipe is not occupied)
+      // skip zero operator blocks: a warp-uniform branch per 32-column block, then per
+      // 8-column group (whole 16-row k-tile each, so the tensor pipe is not occupied).
+      // Fully dense blocks and dense column pairs interleave their column groups with
+      // k4 outermost, so consecutive DMMAs accumulate into different registers.
+      const double *bw = &sm.B[st][gc][wn * BN + gr];
 #pragma unroll
       for (int grp = 0; grp < 3; ++grp) {
-        if ((m12 >> (4 * grp)) & 0xFu) {
+        const unsigned m4 = (m12 >> (4 * grp)) & 0xFu;
+        if (m4 == 0xFu) {
+          mma_cols<4, BST>(acc, a, bw, grp * 4);
+        } else if (m4) {
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            if ((m12 >> (4 * grp + jj)) & 1u) {
-#pragma unroll
-              for (int k4 = 0; k4 < BK / 4; ++k4) {
-                const double b = sm.B[st][k4 * 4 + gc][wn * BN + grp * 32 + jj * 8 + gr];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) dmma(acc[grp * 4 + jj][i][0], acc[grp * 4 + jj][i][1], a[k4][i], b);
-              }
+          for (int pr = 0; pr < 2; ++pr) {
+            const unsigned m2 = (m4 >> (2 * pr)) & 3u;
+            if (m2 == 3u) {
+              mma_cols<2, BST>(acc, a, bw, grp * 4 + 2 * pr);
+            } else if (m2 == 1u) {
+              mma_cols<1, BST>(acc, a, bw, grp * 4 + 2 * pr);
+            } else if (m2 == 2u) {
+              mma_cols<1, BST>(acc, a, bw, grp * 4 + 2 * pr + 1);
             }
           }
         }
