@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         double *row = g.tr + e * (int64_t)g.ncols;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
-          const int col = n0 + wn * BN + j * 8 + 2 * gc;
+          const int col = n0 + (j * NH + wn) * 8 + 2 * gc;   // warp columns alternate 8-column groups
           double v0 = acc[j][i][0], v1 = acc[j][i][1];
           if (g.scale) {   // point values: quadrature weight / material at the point
             const double *sc = g.scale + e * g.sQ;

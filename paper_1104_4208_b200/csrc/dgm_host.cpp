@@ -365,6 +365,16 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   };
   clean(B1);
   clean(B2);
+  // operator column of CTA-tile column tc (warp column h = tc / 96) of n-tile t.
+  // Stage type (gather): the three component blocks of modes [32(nh t + h), +32).
+  // Trace type: the warp columns take the tile's 8-column groups alternately, so both
+  // see the same mix of dense and sparse output columns (the per-face trace operators
+  // differ a lot in density; contiguous halves left one warp column with 2-3x the
+  // blocks of the other at p >= 8)
+  auto tile_col = [&](int t, int tc, bool gather, int bnt) {
+    const int nh = bnt / BN, h = tc / BN, t3 = tc % BN;
+    return gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + ((t3 / 8) * nh + h) * 8 + t3 % 8;
+  };
   // per n-tile: non-zero k-tiles with the mask of non-zero 16x8 column groups
   constexpr int GW = 8;   // 16x8 blocks (one MMA column group); 12 mask bits per k-tile
   auto tiles = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int klo, int khi,
@@ -372,15 +382,13 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     ktl.clear();
     ktoff.assign(1, 0);
     const int bnt = bnt_arg > 0 ? bnt_arg : BNT;
-    const int nh = bnt / BN;
     for (int t = 0; t < ntn; ++t) {
       for (int kt = klo / BK; kt < khi / BK; ++kt) {
         uint32_t mask = 0;   // 12 bits per warp column: its non-zero 16x8 groups
         for (int grp = 0; grp < bnt / GW; ++grp)
           for (int cc = 0; cc < GW && !(mask >> grp & 1); ++cc) {
             const int tc = grp * GW + cc;   // column within the CTA tile; warp column h = tc / 96
-            const int h = tc / BN, t3 = tc % BN;
-            const int col = gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + tc;
+            const int col = tile_col(t, tc, gather, bnt);
             for (int k = kt * BK; k < (kt + 1) * BK; ++k)
               if (B[(size_t)k * nc + col] != 0.0) {
                 mask |= 1u << grp;
@@ -393,17 +401,16 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     }
   };
   // pre-tiled operator pool [n-tile][k-tile][BK][bnt + 4]: every (n-tile, k-tile) tile
-  // in the GEMM's shared-memory layout (same column gather as `tiles`), so a k-tile
+  // in the GEMM's shared-memory layout (same columns as `tiles`: tile_col), so a k-tile
   // load is one linear copy
   auto pool = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int bnt) {
-    const int nh = bnt / BN, bst = bnt + 4, nkt = (int)(B.size() / nc) / BK;
+    const int bst = bnt + 4, nkt = (int)(B.size() / nc) / BK;
     std::vector<double> P((size_t)ntn * nkt * BK * bst, 0.0);
     for (int t = 0; t < ntn; ++t)
       for (int kt = 0; kt < nkt; ++kt)
         for (int r = 0; r < BK; ++r)
           for (int tc = 0; tc < bnt; ++tc) {
-            const int h = tc / BN, t3 = tc % BN;
-            const int col = gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + tc;
+            const int col = tile_col(t, tc, gather, bnt);
             P[(((size_t)t * nkt + kt) * BK + r) * bst + tc] = B[(size_t)(kt * BK + r) * nc + col];
           }
     return P;
@@ -443,8 +450,17 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
       for (uint32_t x : l) n += __builtin_popcount(x >> 8);
       return n;
     };
-    std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x32)\n", c->p,
+    std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x8)\n", c->p,
                  l1[0][3].size(), bits(l1[0][3]), l2[0].size(), bits(l2[0]));
+    // per trace n-tile: k-tiles and 16x8 blocks of each warp column (load balance)
+    for (size_t t = 0; t + 1 < o2[0].size(); ++t) {
+      long w0 = 0, w1 = 0;
+      for (int i = o2[0][t]; i < o2[0][t + 1]; ++i) {
+        w0 += __builtin_popcount((l2[0][i] >> 8) & 0xFFFu);
+        w1 += __builtin_popcount((l2[0][i] >> 20) & 0xFFFu);
+      }
+      std::fprintf(stderr, "  B2 n-tile %zu: %d k-tiles, blocks %ld | %ld\n", t, o2[0][t + 1] - o2[0][t], w0, w1);
+    }
   }
   std::vector<double> P1[2], P2[2];
   for (int v = 0; v < nvar; ++v) {
