@@ -307,6 +307,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   const int N = c->N, NF = c->NF;
   constexpr int NH = dgm::kDenseNH1, BNT = BN * NH;
   c->dense.trace_nh = c->p >= 8 ? 2 : 1;   // measured: wider trace tiles win from p = 8
+  if (const char *v = std::getenv("DGM_TRACE_NH"))   // measurement override (1 or 2)
+    if (std::atoi(v) == 1 || std::atoi(v) == 2) c->dense.trace_nh = std::atoi(v);
   const int BNT2 = BN * c->dense.trace_nh;
   const int Nk = (N + BK - 1) / BK * BK, NFk = (NF + BK - 1) / BK * BK, Np = (N + 32 * NH - 1) / (32 * NH) * (32 * NH);
   const int k1a = 3 * Nk;
