@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         }
       }
       __syncthreads();
-      constexpr int MODES = BNT / 3;   // 32 NH modes, warp column h holds modes [32h, 32h+32)
+      constexpr int MODES = BNT / 3;   // 32 NH modes; the warp columns alternate 8-mode groups
       constexpr int U = 4;   // items per batch: their 3U loads are in flight together
       const int64_t cs = g.n_tet * g.LD;
       const bool upd = g.out_mode == OUT_UPDATE;
@@ -366,7 +366,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const int r = idx / MODES, ml = idx - r * MODES;
           const double *G = Gs[r];
           const double cm = G[6];
-          const int hb = (ml >> 5) * BN + (ml & 31);
+          // tile mode ml -> warp column h = (ml/8) % NH, its mode ((ml/8)/NH) 8 + ml%8
+          const int hb = ((ml >> 3) % NH) * BN + ((ml >> 3) / NH) * 8 + (ml & 7);
           const double v0 = Cs[r][hb], v1 = Cs[r][32 + hb], v2 = Cs[r][64 + hb];
           if (g.raw) {   // residual before the (variable-material) inverse mass
             double *rw = g.raw + (m0 + r) * (int64_t)g.rawld + 32 * NH * nt + ml;
@@ -502,7 +503,7 @@ dgm_status gemm_go_nh(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
 // context's choice (two warp columns halve the A re-reads at p >= 8)
 template <int EPI>
 dgm_status gemm_go(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
-  if (EPI == EPI_TRACE && c->dense.trace_nh == 2) return gemm_go_nh<EPI, 2>(c, g, st);
+  if ((EPI == EPI_TRACE ? c->dense.trace_nh : c->dense.stage_nh) == 2) return gemm_go_nh<EPI, 2>(c, g, st);
   return gemm_go_nh<EPI, 1>(c, g, st);
 }
 
@@ -540,7 +541,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
   g.ktl = D.ktl1[v][sel];
   g.ktoff = D.ktoff1[v][sel];
-  g.ntiles_n = D.nc1 / 3 / (32 * kDenseNH1);
+  g.ntiles_n = D.nc1 / 3 / (32 * D.stage_nh);
   g.n_tet = c->n_tet;
   g.N = c->N;
   g.NF = c->NF;

@@ -305,7 +305,13 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   static const double T1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
   static const double T2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
   const int N = c->N, NF = c->NF;
-  constexpr int NH = dgm::kDenseNH1, BNT = BN * NH;
+  // two warp columns for the stage GEMMs where that adds no mode padding (N rounds up
+  // to the same multiple of 32 and 64) from p = 8: C4 7.60 -> 6.87 ms; p = 7 and the
+  // padded orders (6, 9, 10) measured slower
+  c->dense.stage_nh = (c->p >= 8 && (c->N + 31) / 32 * 32 == (c->N + 63) / 64 * 64) ? 2 : 1;
+  if (const char *v = std::getenv("DGM_STAGE_NH"))   // measurement override (1 or 2)
+    if (std::atoi(v) == 1 || std::atoi(v) == 2) c->dense.stage_nh = std::atoi(v);
+  const int NH = c->dense.stage_nh, BNT = BN * NH;
   c->dense.trace_nh = c->p >= 8 ? 2 : 1;   // measured: wider trace tiles win from p = 8
   if (const char *v = std::getenv("DGM_TRACE_NH"))   // measurement override (1 or 2)
     if (std::atoi(v) == 1 || std::atoi(v) == 2) c->dense.trace_nh = std::atoi(v);
@@ -368,14 +374,17 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   clean(B1);
   clean(B2);
   // operator column of CTA-tile column tc (warp column h = tc / 96) of n-tile t.
-  // Stage type (gather): the three component blocks of modes [32(nh t + h), +32).
+  // Stage type (gather): the three component blocks of the tile's 32 nh modes, the warp
+  // columns taking alternate 8-mode groups (nh = 2).
   // Trace type: the warp columns take the tile's 8-column groups alternately, so both
   // see the same mix of dense and sparse output columns (the per-face trace operators
   // differ a lot in density; contiguous halves left one warp column with 2-3x the
   // blocks of the other at p >= 8)
   auto tile_col = [&](int t, int tc, bool gather, int bnt) {
     const int nh = bnt / BN, h = tc / BN, t3 = tc % BN;
-    return gather ? (t3 / 32) * Np + 32 * (nh * t + h) + t3 % 32 : t * bnt + ((t3 / 8) * nh + h) * 8 + t3 % 8;
+    const int lm = t3 % 32;   // stage type: mode of the warp column; tile mode (lm/8 nh + h) 8 + lm%8
+    return gather ? (t3 / 32) * Np + 32 * nh * t + ((lm / 8) * nh + h) * 8 + lm % 8
+                  : t * bnt + ((t3 / 8) * nh + h) * 8 + t3 % 8;
   };
   // per n-tile: non-zero k-tiles with the mask of non-zero 16x8 column groups
   constexpr int GW = 8;   // 16x8 blocks (one MMA column group); 12 mask bits per k-tile

@@ -80,10 +80,6 @@ struct DevStream {
 // 32).  B2 [3Nk][nc2]: rows c*Nk+β, columns (f*2+k)*NF+γ (trace-buffer order).
 // ktl/ktoff: per n-tile the non-zero k-tiles with a 12-bit mask of non-zero 16x8
 // column groups (sel 1 curl only, 2 flux only, 3 both).
-// warp columns per dense GEMM CTA (CTA tile = 64 elements x 96*NH columns): the stage
-// GEMMs (gathered component blocks) use 1, the trace-type GEMMs (contiguous columns) 2;
-// the host pads the operator layouts to them
-constexpr int kDenseNH1 = 1;
 // Per updated field v (0: E stage / E traces, 1: H stage / H traces) a variant of the
 // matrices; they differ only for mixed orders (H ∈ P^{p-1}: B1[0] ignores H's modes
 // >= N(p-1) as curl input, B1[1] has no output columns there, B2[1] no rows there).
@@ -94,7 +90,12 @@ struct DenseOps {
   double *B1[2] = {nullptr, nullptr}, *B2[2] = {nullptr, nullptr}, *AB = nullptr;
   int nc1 = 0, nc2 = 0, k1a = 0;
   int nkt1 = 0, nkt2 = 0, nktf = 0, nktb = 0;   // k-tiles of B1, B2, Bf, Bb (pool strides)
-  int trace_nh = 1;   // warp columns of the trace-type GEMMs (B2, Bf): 2 for p >= 8
+  // warp columns per GEMM CTA (CTA tile = 64 elements x 96 NH columns); the host pads
+  // the operator layouts to them. Stage type (B1, Bb): NH = 1 takes the three component
+  // blocks of 32 modes, NH = 2 of 64 modes, the warp columns alternating 8-mode groups.
+  // Trace type (B2, Bf): contiguous columns, warp columns alternating 8-column groups.
+  int stage_nh = 1;
+  int trace_nh = 1;   // 2 for p >= 8
   uint32_t *ktl1[2][4] = {};
   int32_t *ktoff1[2][4] = {};
   uint32_t *ktl2[2] = {nullptr, nullptr};
