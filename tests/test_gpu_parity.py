@@ -359,3 +359,16 @@ def test_step_capturable_into_user_graph():
     g.replay()
     torch.cuda.synchronize()
     assert bool((E1 == E2).all()) and bool((H1 == H2).all())
+
+
+@pytest.mark.parametrize("stage_nh,trace_nh", [(1, 1), (2, 2), (2, 1), (1, 2)])
+@pytest.mark.parametrize("case,p", [("pec-upwind", 3), ("mixed-upwind", 6), ("periodic-central", 8),
+                                    ("pec-central", 10)])
+def test_dense_warp_column_layouts(case, p, stage_nh, trace_nh, monkeypatch):
+    """Dense engine with each GEMM tile layout forced (DGM_STAGE_NH / DGM_TRACE_NH; the
+    default picks by order, include/dgm.h): one or two warp columns, the second with
+    interleaved 8-column groups and, for the stage GEMMs, 64-mode padding."""
+    monkeypatch.setenv("DGM_STAGE_NH", str(stage_nh))
+    monkeypatch.setenv("DGM_TRACE_NH", str(trace_nh))
+    errs = _apply_parity(case, p, "dense")
+    assert max(errs.values()) <= TOL_APPLY, errs
