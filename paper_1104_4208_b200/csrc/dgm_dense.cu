@@ -136,20 +136,22 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// NJ consecutive 8-column groups j0.. of one k-tile: k4 outermost, so the 2 NJ
-// DMMAs of one k4 step are independent (hides the DMMA dependency latency)
-template <int NJ, int BST>
-__device__ __forceinline__ void mma_cols(double (&acc)[12][2][2], const double (&a)[BK / 4][2], const double *bw,
-                                         int j0) {
+// the 8-column groups j0 + j of one k-tile for the set bits j of M: k4 outermost, so
+// the DMMAs of one k4 step are independent (hides the DMMA dependency latency)
+template <unsigned M, int BST>
+__device__ __forceinline__ void mma_set(double (&acc)[12][2][2], const double (&a)[BK / 4][2], const double *bw,
+                                        int j0) {
 #pragma unroll
   for (int k4 = 0; k4 < BK / 4; ++k4) {
-    double b[NJ];
+    double b[4];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) b[j] = bw[k4 * 4 * BST + (j0 + j) * 8];
+    for (int j = 0; j < 4; ++j)
+      if (M >> j & 1u) b[j] = bw[k4 * 4 * BST + (j0 + j) * 8];
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
+    for (int j = 0; j < 4; ++j)
+      if (M >> j & 1u)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) dmma(acc[j0 + j][i][0], acc[j0 + j][i][1], a[k4][i], b[j]);
+        for (int i = 0; i < 2; ++i) dmma(acc[j0 + j][i][0], acc[j0 + j][i][1], a[k4][i], b[j]);
   }
 }
 
@@ -267,28 +269,20 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
       const unsigned m12 = (kcur >> (8 + 12 * wn)) & 0xFFFu;   // this warp column's non-zero 16x8 groups
       kcur = knext;
-      // skip zero operator blocks: a warp-uniform branch per 32-column block, then per
-      // 8-column group (whole 16-row k-tile each, so the tensor pipe is not occupied).
-      // Fully dense blocks and dense column pairs interleave their column groups with
-      // k4 outermost, so consecutive DMMAs accumulate into different registers.
+      // skip zero operator blocks: per 32-column block a warp-uniform switch over its
+      // mask of non-zero 8-column groups (whole 16-row k-tiles, so the tensor pipe is not
+      // occupied); the non-zero groups run interleaved with k4 outermost, so
+      // consecutive DMMAs accumulate into different registers
       const double *bw = &sm.B[st][gc][wn * BN + gr];
 #pragma unroll
       for (int grp = 0; grp < 3; ++grp) {
-        const unsigned m4 = (m12 >> (4 * grp)) & 0xFu;
-        if (m4 == 0xFu) {
-          mma_cols<4, BST>(acc, a, bw, grp * 4);
-        } else if (m4) {
-#pragma unroll
-          for (int pr = 0; pr < 2; ++pr) {
-            const unsigned m2 = (m4 >> (2 * pr)) & 3u;
-            if (m2 == 3u) {
-              mma_cols<2, BST>(acc, a, bw, grp * 4 + 2 * pr);
-            } else if (m2 == 1u) {
-              mma_cols<1, BST>(acc, a, bw, grp * 4 + 2 * pr);
-            } else if (m2 == 2u) {
-              mma_cols<1, BST>(acc, a, bw, grp * 4 + 2 * pr + 1);
-            }
-          }
+        switch ((m12 >> (4 * grp)) & 0xFu) {
+#define DGM_SET(M) \
+  case M: mma_set<M, BST>(acc, a, bw, grp * 4); break;
+          DGM_SET(1) DGM_SET(2) DGM_SET(3) DGM_SET(4) DGM_SET(5) DGM_SET(6) DGM_SET(7) DGM_SET(8)
+          DGM_SET(9) DGM_SET(10) DGM_SET(11) DGM_SET(12) DGM_SET(13) DGM_SET(14) DGM_SET(15)
+#undef DGM_SET
+          default: break;
         }
       }
     }
