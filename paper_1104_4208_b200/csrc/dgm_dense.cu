@@ -63,14 +63,16 @@ struct GemmArgs {
   // k-tile geometry: k-tiles per A block below / above k1 (and float reciprocals)
   int k1t, nkA, nkF;
   float rnkA, rnkF;
-  // B operand: pre-tiled pool [ntiles_n][nkt][BK][BST] (host: dense_build tile_pool);
-  // per n-tile the list of non-zero k-tiles
+  // B operand: pre-tiled pool [ntiles_n][nkt][BK][BST] (host: dense_build, `pool`),
+  // columns as `tile_col` there: EPI_STAGE gathers the three component blocks of the
+  // tile's 32 NH modes (warp columns alternate 8-mode groups); EPI_TRACE takes
+  // contiguous columns (warp columns alternate 8-column groups)
   const double *Bm;
   int nkt;
   int NC;
-  int Np;                  // EPI_STAGE: column m*Np + β (component-blocked); tile t, warp column h gathers
-                           // β in [32(NH t + h), +32)
-  const uint32_t *ktl;     // per non-zero k-tile: kt | (3NH-bit mask of non-zero 16x32 column blocks) << 16
+  int Np;                  // operator columns per component (EPI_STAGE: column m*Np + β)
+  const uint32_t *ktl;     // per non-zero k-tile: kt | (12-bit mask of non-zero 16x8 column groups per
+                           // warp column, warp column h at bit 12h) << 8
   const int32_t *ktoff;
   int ntiles_n;
   int64_t n_tet;
