@@ -77,7 +77,7 @@ struct DevStream {
 // from the exact programs.  Rows are component-blocked and padded to the k-tile
 // (Nk = N, NFk = NF rounded up to 16).  B1 [3Nk+8NFk][3Np]: rows c*Nk+β (curl input),
 // k1a + j*NFk + γ (face field j = f*2+{A,B}); columns m*Np+β (Np = N rounded up to
-// 32).  B2 [3Nk][nc2]: rows c*Nk+β, columns (f*2+k)*NF+γ (trace-buffer order).
+// 32 stage_nh).  B2 [3Nk][nc2]: rows c*Nk+β, columns (f*2+k)*NF+γ (trace-buffer order).
 // ktl/ktoff: per n-tile the non-zero k-tiles with a 12-bit mask per warp column of non-zero 16x8
 // column groups (sel 1 curl only, 2 flux only, 3 both).
 // Per updated field v (0: E stage / E traces, 1: H stage / H traces) a variant of the
