@@ -47,7 +47,7 @@ struct Cfg {
   };
   static constexpr size_t EPI_BYTES = sizeof(double) * (BM_ * (BN * NH_ + 4) + BM_ * 8);   // C tile + geometry
   static constexpr size_t SMEM_DATA = sizeof(Smem) > EPI_BYTES ? sizeof(Smem) : EPI_BYTES;
-  static constexpr size_t SMEM = SMEM_DATA + 8 * NST_;   // + one mbarrier per stage (B tile)
+  static constexpr size_t SMEM = SMEM_DATA + 8 * NST_ + 8;   // + one mbarrier per stage (B tile), next tile
 };
 
 enum { EPI_STAGE = 0, EPI_TRACE = 1 };
@@ -92,6 +92,7 @@ struct GemmArgs {
   double *raw;
   int rawld, rawNk;
   int unit_m;
+  unsigned long long *tile_ctr;   // dynamic tile counter (zeroed before the launch), or null: static order
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -215,7 +216,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
   const int64_t mtiles = (g.n_tet + BM - 1) / BM;
   const int64_t ntile_total = mtiles * g.ntiles_n;
-  for (int64_t t = blockIdx.x; t < ntile_total; t += gridDim.x) {
+  // dynamic tile order: CTAs take tiles in sequence from a counter (reset before each
+  // launch), so the n-tiles of one m-tile start together and share its A rows in L2
+  long long *tnext = reinterpret_cast<long long *>(dsm + C::SMEM_DATA + 8 * NSTAGE);
+  for (int64_t t = blockIdx.x; t < ntile_total;) {
     const int64_t m0 = (t / g.ntiles_n) * BM;
     const int nt = (int)(t % g.ntiles_n);
     const int n0 = nt * BNT;
@@ -382,7 +386,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
         }
       }
     }
+    if (tid == 0) *tnext = g.tile_ctr ? (long long)atomicAdd(g.tile_ctr, 1ull) + gridDim.x : t + gridDim.x;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // epilogue writes before the next bulk copies
+    __syncthreads();
+    t = *tnext;
     __syncthreads();
   }
 }
@@ -460,6 +467,7 @@ __global__ void dense_flux_kernel(StageArgs a, const double *__restrict__ trY, d
 template <int EPI, class C>
 dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g0, cudaStream_t st) {
   GemmArgs g = g0;
+  g.tile_ctr = c->dense.tile_ctr;
   g.k1t = g.k1 / BK;
   g.nkA = g.Nk / BK;
   g.nkF = g.NFk / BK;
@@ -474,6 +482,8 @@ dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g0, cudaStream_t st) {
   const int64_t tiles = (g.n_tet + C::BM - 1) / C::BM * g.ntiles_n;
   int64_t grid = (int64_t)c->sms * occ;
   if (grid > tiles) grid = tiles;
+  if (g.tile_ctr && cudaMemsetAsync(g.tile_ctr, 0, sizeof(unsigned long long), st) != cudaSuccess)
+    return set_err(c, DGM_ECUDA, "gemm tile counter reset");
   kern<<<(unsigned)grid, C::NTHREADS, smem, st>>>(g);
   c->launches++;
   cudaError_t e = cudaGetLastError();

@@ -562,6 +562,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     CUDA_TRY(c, cudaMalloc(&D.P, sizeof(double) * 3 * (size_t)Qk * (size_t)(n_or1(c))));
   }
   CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NFk * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
+  if (!(std::getenv("DGM_TILE_ORDER") && std::atoi(std::getenv("DGM_TILE_ORDER")) == 0))   // 0: static order
+    CUDA_TRY(c, cudaMalloc(&D.tile_ctr, 64));
   return DGM_OK;
 }
 
@@ -573,6 +575,7 @@ void free_ctx(dgm_ctx *c) {
     if (c->gev[i]) cudaEventDestroy(c->gev[i]);
   cudaFree(c->d_dense);
   cudaFree(c->dense.AB);
+  cudaFree(c->dense.tile_ctr);
   for (void *q : {(void *)c->dense.Bf, (void *)c->dense.Bb, (void *)c->dense.ktlf, (void *)c->dense.ktofff,
                   (void *)c->dense.ktlb, (void *)c->dense.ktoffb, (void *)c->dense.SWe, (void *)c->dense.SWm,
                   (void *)c->dense.AC, (void *)c->dense.P})

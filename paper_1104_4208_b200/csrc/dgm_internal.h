@@ -95,6 +95,7 @@ struct DenseOps {
   // blocks of 32 modes, NH = 2 of 64 modes, the warp columns alternating 8-mode groups.
   // Trace type (B2, Bf): contiguous columns, warp columns alternating 8-column groups.
   int stage_nh = 1;
+  unsigned long long *tile_ctr = nullptr;   // GEMM dynamic tile counter (null: static tile order)
   int trace_nh = 1;   // 2 for p >= 8
   uint32_t *ktl1[2][4] = {};
   int32_t *ktoff1[2][4] = {};
