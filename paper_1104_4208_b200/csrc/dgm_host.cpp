@@ -305,14 +305,14 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   static const double T1[4][3] = {{-1, 1, 0}, {0, 1, 0}, {1, 0, 0}, {1, 0, 0}};
   static const double T2[4][3] = {{-1, 0, 1}, {0, 0, 1}, {0, 0, 1}, {0, 1, 0}};
   const int N = c->N, NF = c->NF;
-  // two warp columns for the stage GEMMs where that adds no mode padding (N rounds up
-  // to the same multiple of 32 and 64) from p = 8: C4 7.60 -> 6.87 ms; p = 7 and the
-  // padded orders (6, 9, 10) measured slower
-  c->dense.stage_nh = (c->p >= 8 && (c->N + 31) / 32 * 32 == (c->N + 63) / 64 * 64) ? 2 : 1;
+  // one warp column for every GEMM: with the dynamic tile order the CTAs of one m-tile
+  // share its A rows in L2, and two warp columns (one A tile for 192 columns) measured
+  // slower at every order; the overrides keep both layouts testable
+  c->dense.stage_nh = 1;
   if (const char *v = std::getenv("DGM_STAGE_NH"))   // measurement override (1 or 2)
     if (std::atoi(v) == 1 || std::atoi(v) == 2) c->dense.stage_nh = std::atoi(v);
   const int NH = c->dense.stage_nh, BNT = BN * NH;
-  c->dense.trace_nh = c->p >= 8 ? 2 : 1;   // measured: wider trace tiles win from p = 8
+  c->dense.trace_nh = 1;
   if (const char *v = std::getenv("DGM_TRACE_NH"))   // measurement override (1 or 2)
     if (std::atoi(v) == 1 || std::atoi(v) == 2) c->dense.trace_nh = std::atoi(v);
   const int BNT2 = BN * c->dense.trace_nh;

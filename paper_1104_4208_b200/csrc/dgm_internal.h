@@ -96,7 +96,7 @@ struct DenseOps {
   // Trace type (B2, Bf): contiguous columns, warp columns alternating 8-column groups.
   int stage_nh = 1;
   unsigned long long *tile_ctr = nullptr;   // GEMM dynamic tile counter (null: static tile order)
-  int trace_nh = 1;   // 2 for p >= 8
+  int trace_nh = 1;
   uint32_t *ktl1[2][4] = {};
   int32_t *ktoff1[2][4] = {};
   uint32_t *ktl2[2] = {nullptr, nullptr};
