@@ -90,7 +90,7 @@ typedef struct {
  * The environment variable DGM_ENGINE=sparse|dense overrides AUTO.  For measurements,
  * DGM_STAGE_NH / DGM_TRACE_NH = 1|2 force the dense GEMM tile width (one or two 96-column
  * warp columns; default one) and DGM_TILE_ORDER=0 the static GEMM tile order
- * (default: dynamic, from a per-context counter, so one context must not run dense GEMMs
+ * (default: dynamic, from a per-context self-resetting counter, so one context must not run dense GEMMs
  * on two streams at once); results are the same operator. */
 typedef enum { DGM_ENGINE_AUTO = 0, DGM_ENGINE_SPARSE = 1, DGM_ENGINE_DENSE = 2 } dgm_engine_kind;
 

@@ -71,8 +71,8 @@ struct GemmArgs {
   int nkt;
   int NC;
   int Np;                  // operator columns per component (EPI_STAGE: column m*Np + β)
-  const uint32_t *ktl;     // per non-zero k-tile: kt | (12-bit mask of non-zero 16x8 column groups per
-                           // warp column, warp column h at bit 12h) << 8
+  const uint64_t *ktl;     // per non-zero k-tile: kt | (12-bit mask of non-zero 16x8 column groups per
+                           // warp column, warp column h at bit 12h) << 16
   const int32_t *ktoff;
   int ntiles_n;
   int64_t n_tet;
@@ -92,7 +92,7 @@ struct GemmArgs {
   double *raw;
   int rawld, rawNk;
   int unit_m;
-  unsigned long long *tile_ctr;   // dynamic tile counter (zeroed before the launch), or null: static order
+  unsigned long long *tile_ctr;   // dynamic tile counter [claims, arrivals] (self-resetting), or null: static order
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -216,14 +216,14 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
   const int gr = lane >> 2, gc = lane & 3;   // fragment row / k index
   const int64_t mtiles = (g.n_tet + BM - 1) / BM;
   const int64_t ntile_total = mtiles * g.ntiles_n;
-  // dynamic tile order: CTAs take tiles in sequence from a counter (reset before each
-  // launch), so the n-tiles of one m-tile start together and share its A rows in L2
+  // dynamic tile order: CTAs take tiles in sequence from a counter (zeroed by the last
+  // CTA of the previous launch), so the n-tiles of one m-tile start together and share its A rows in L2
   long long *tnext = reinterpret_cast<long long *>(dsm + C::SMEM_DATA + 8 * NSTAGE);
   for (int64_t t = blockIdx.x; t < ntile_total;) {
     const int64_t m0 = (t / g.ntiles_n) * BM;
     const int nt = (int)(t % g.ntiles_n);
     const int n0 = nt * BNT;
-    const uint32_t *kts = g.ktl + g.ktoff[nt];
+    const uint64_t *kts = g.ktl + g.ktoff[nt];
     const int nk = g.ktoff[nt + 1] - g.ktoff[nt];
     double acc[12][2][2];   // [column group j][row group i][pair]
 #pragma unroll
@@ -254,26 +254,26 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     // prologue
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
-      if (s < nk) load_tile<EPI, C>(g, sm, mbar, s, ar, nt, (int)(kts[s] & 0xFFu), tid);
+      if (s < nk) load_tile<EPI, C>(g, sm, mbar, s, ar, nt, (int)(kts[s] & 0xFFFFu), tid);
       cp_commit();
     }
-    uint32_t kcur = nk > 0 ? kts[0] : 0u;
+    uint64_t kcur = nk > 0 ? kts[0] : 0ull;
     for (int it = 0; it < nk; ++it) {
-      const uint32_t knext = it + 1 < nk ? kts[it + 1] : 0u;   // one ahead: off the critical path
+      const uint64_t knext = it + 1 < nk ? kts[it + 1] : 0ull;   // one ahead: off the critical path
       const int st = it % NSTAGE;
       cp_wait<NSTAGE - 2>();
       mbar_wait(&mbar[st], (ph >> st) & 1u);
       ph ^= 1u << st;
       __syncthreads();
       const int nx = it + NSTAGE - 1;
-      if (nx < nk) load_tile<EPI, C>(g, sm, mbar, nx % NSTAGE, ar, nt, (int)(kts[nx] & 0xFFu), tid);
+      if (nx < nk) load_tile<EPI, C>(g, sm, mbar, nx % NSTAGE, ar, nt, (int)(kts[nx] & 0xFFFFu), tid);
       cp_commit();
       double a[BK / 4][2];
 #pragma unroll
       for (int k4 = 0; k4 < BK / 4; ++k4)
 #pragma unroll
         for (int i = 0; i < 2; ++i) a[k4][i] = sm.A[st][wm * WM + i * 8 + gr][k4 * 4 + gc];
-      const unsigned m12 = (kcur >> (8 + 12 * wn)) & 0xFFFu;   // this warp column's non-zero 16x8 groups
+      const unsigned m12 = (unsigned)(kcur >> (16 + 12 * wn)) & 0xFFFu;   // this warp column's non-zero 16x8 groups
       kcur = knext;
       // skip zero operator blocks: per 32-column block a warp-uniform switch over its
       // mask of non-zero 8-column groups (whole 16-row k-tiles, so the tensor pipe is not
@@ -392,6 +392,16 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
     t = *tnext;
     __syncthreads();
   }
+  // self-resetting tile counter: the last CTA to finish zeroes it for the next launch
+  // (every CTA's claims on ctr[0] precede its arrival on ctr[1])
+  if (g.tile_ctr && tid == 0) {
+    __threadfence();
+    if (atomicAdd(g.tile_ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+      g.tile_ctr[0] = 0ull;
+      g.tile_ctr[1] = 0ull;
+      __threadfence();
+    }
+  }
 }
 
 // A, B face fields of every (element, face, mode) from the trace buffers
@@ -482,8 +492,6 @@ dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g0, cudaStream_t st) {
   const int64_t tiles = (g.n_tet + C::BM - 1) / C::BM * g.ntiles_n;
   int64_t grid = (int64_t)c->sms * occ;
   if (grid > tiles) grid = tiles;
-  if (g.tile_ctr && cudaMemsetAsync(g.tile_ctr, 0, sizeof(unsigned long long), st) != cudaSuccess)
-    return set_err(c, DGM_ECUDA, "gemm tile counter reset");
   kern<<<(unsigned)grid, C::NTHREADS, smem, st>>>(g);
   c->launches++;
   cudaError_t e = cudaGetLastError();

@@ -389,7 +389,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   // per n-tile: non-zero k-tiles with the mask of non-zero 16x8 column groups
   constexpr int GW = 8;   // 16x8 blocks (one MMA column group); 12 mask bits per k-tile
   auto tiles = [&](const std::vector<double> &B, int nc, int ntn, bool gather, int klo, int khi,
-                   std::vector<uint32_t> &ktl, std::vector<int32_t> &ktoff, int bnt_arg = 0) {
+                   std::vector<uint64_t> &ktl, std::vector<int32_t> &ktoff, int bnt_arg = 0) {
     ktl.clear();
     ktoff.assign(1, 0);
     const int bnt = bnt_arg > 0 ? bnt_arg : BNT;
@@ -406,7 +406,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
                 break;
               }
           }
-        if (mask) ktl.push_back((uint32_t)kt | (mask << 8));   // kt < 256: K <= 4096 rows
+        if (mask) ktl.push_back((uint64_t)kt | ((uint64_t)mask << 16));   // kt < 65536
       }
       ktoff.push_back((int32_t)ktl.size());
     }
@@ -447,7 +447,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
       for (int m = 0; m < 3; ++m)
         for (int b = NHm; b < Np; ++b) B1v[1][k * nc1 + (size_t)m * Np + b] = 0.0;   // H outputs
   }
-  std::vector<uint32_t> l1[2][4], l2[2];
+  std::vector<uint64_t> l1[2][4], l2[2];
   std::vector<int32_t> o1[2][4], o2[2];
   for (int v = 0; v < nvar; ++v) {
     tiles(B1v[v], nc1, Np / (32 * NH), true, 0, k1a, l1[v][1], o1[v][1]);
@@ -456,9 +456,9 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     tiles(B2v[v], nc2, nc2 / BNT2, false, 0, K2, l2[v], o2[v], BNT2);
   }
   if (std::getenv("DGM_DEBUG_DENSE")) {
-    auto bits = [](const std::vector<uint32_t> &l) {
+    auto bits = [](const std::vector<uint64_t> &l) {
       long n = 0;
-      for (uint32_t x : l) n += __builtin_popcount(x >> 8);
+      for (uint64_t x : l) n += __builtin_popcountll(x >> 16);
       return n;
     };
     std::fprintf(stderr, "dense_build p=%d: B1 %zu k-tiles %ld blocks, B2 %zu k-tiles %ld blocks (16x8)\n", c->p,
@@ -500,10 +500,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     D.B1[v] = (double *)put(P1[v].data(), P1[v].size() * 8);
     D.B2[v] = (double *)put(P2[v].data(), P2[v].size() * 8);
     for (int i = 1; i < 4; ++i) {
-      D.ktl1[v][i] = (uint32_t *)put(l1[v][i].data(), l1[v][i].size() * 4);
+      D.ktl1[v][i] = (uint64_t *)put(l1[v][i].data(), l1[v][i].size() * 8);
       D.ktoff1[v][i] = (int32_t *)put(o1[v][i].data(), o1[v][i].size() * 4);
     }
-    D.ktl2[v] = (uint32_t *)put(l2[v].data(), l2[v].size() * 4);
+    D.ktl2[v] = (uint64_t *)put(l2[v].data(), l2[v].size() * 8);
     D.ktoff2[v] = (int32_t *)put(o2[v].data(), o2[v].size() * 4);
   }
   if (!ok) return dgm::set_err(c, DGM_ECUDA, "dense_build: upload failed");
@@ -539,7 +539,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
           Bf[(size_t)(cc * Nk + b) * ncf + cc * Qk + i] = Phi[(size_t)i * N + b];
           Bb[(size_t)(cc * Qk + i) * nc1 + (size_t)cc * Np + b] = Phi[(size_t)i * N + b] / hs.norms[b];
         }
-    std::vector<uint32_t> lf, lb;
+    std::vector<uint64_t> lf, lb;
     std::vector<int32_t> of, ob;
     tiles(Bf, ncf, ncf / BNT2, false, 0, 3 * Nk, lf, of, BNT2);
     tiles(Bb, nc1, Np / (32 * NH), true, 0, 3 * Qk, lb, ob);
@@ -551,8 +551,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     D.nktf = 3 * Nk / BK;
     D.nktb = 3 * Qk / BK;
     bool okm = up((void **)&D.Bf, Pf.data(), Pf.size() * 8) && up((void **)&D.Bb, Pb.data(), Pb.size() * 8) &&
-               up((void **)&D.ktlf, lf.data(), lf.size() * 4) && up((void **)&D.ktofff, of.data(), of.size() * 4) &&
-               up((void **)&D.ktlb, lb.data(), lb.size() * 4) && up((void **)&D.ktoffb, ob.data(), ob.size() * 4) &&
+               up((void **)&D.ktlf, lf.data(), lf.size() * 8) && up((void **)&D.ktofff, of.data(), of.size() * 4) &&
+               up((void **)&D.ktlb, lb.data(), lb.size() * 8) && up((void **)&D.ktoffb, ob.data(), ob.size() * 4) &&
                up((void **)&D.SWe, c->h_swe.data(), c->h_swe.size() * 8) &&
                up((void **)&D.SWm, c->h_swm.data(), c->h_swm.size() * 8);
     if (!okm) return dgm::set_err(c, DGM_ENOMEM, "dense_build: material-point operators");
@@ -563,7 +563,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   }
   CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NFk * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
   if (!(std::getenv("DGM_TILE_ORDER") && std::atoi(std::getenv("DGM_TILE_ORDER")) == 0))   // 0: static order
+  {
     CUDA_TRY(c, cudaMalloc(&D.tile_ctr, 64));
+    CUDA_TRY(c, cudaMemset(D.tile_ctr, 0, 64));   // then self-resetting (gemm_kernel)
+  }
   return DGM_OK;
 }
 
@@ -1100,7 +1103,9 @@ dgm_status dgm_step_ex(dgm_ctx *c, double *E, double *H, double dt, int64_t nste
 }
 
 dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t nsteps, void *stream) {
-  if (!c || !Eh || !Hh) return dgm::set_err(c, DGM_EINVAL, "null pointer");
+  if (!c || !Eh || !Hh || nsteps < 0 || !std::isfinite(dt)) return dgm::set_err(c, DGM_EINVAL, "bad step arguments");
+  if (c->flux == DGM_FLUX_STABILIZED)   // checked before any copy is enqueued
+    return dgm::set_err(c, DGM_EINVAL, "stabilised contexts step through dgm_step_sc (the face unknowns H^F)");
   cudaStream_t st = (cudaStream_t)stream;
   size_t bytes = sizeof(double) * 3 * (size_t)c->n_tet * c->LD;
   if (!c->d_E) {
@@ -1123,7 +1128,11 @@ dgm_status dgm_step_host(dgm_ctx *c, double *Eh, double *Hh, double dt, int64_t 
   CUDA_TRY(c, cudaEventRecord(c->ev[1], c->side));           // H has arrived
   c->tr_valid = false;   // fresh host data
   dgm_status s = run_steps(c, c->d_E, c->d_H, dt, nsteps, 0, st, c->ev[1], c->ev[2]);
-  if (s != DGM_OK) return s;
+  if (s != DGM_OK) {
+    cudaStreamSynchronize(c->side);   // no copy outlives a failed call
+    cudaStreamSynchronize(st);
+    return s;
+  }
   CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev[2], 0));    // last H stage done
   CUDA_TRY(c, cudaMemcpyAsync(Hh, c->d_H, bytes, cudaMemcpyDeviceToHost, c->side));
   CUDA_TRY(c, cudaEventRecord(c->ev[3], c->side));

@@ -97,15 +97,15 @@ struct DenseOps {
   int stage_nh = 1;
   unsigned long long *tile_ctr = nullptr;   // GEMM dynamic tile counter (null: static tile order)
   int trace_nh = 1;
-  uint32_t *ktl1[2][4] = {};
+  uint64_t *ktl1[2][4] = {};
   int32_t *ktoff1[2][4] = {};
-  uint32_t *ktl2[2] = {nullptr, nullptr};
+  uint64_t *ktl2[2] = {nullptr, nullptr};
   int32_t *ktoff2[2] = {nullptr, nullptr};
   // material points (reverse numerical integration): Bf [3Nk][ncf] residual -> point
   // values, Bb [3Qk][nc1] point values -> modes; SWe/SWm [n][Qk] = ŵ_i / ε, μ at the
   // points; AC [n][3Nk] residual scratch, P [n][3Qk] point-value scratch
   double *Bf = nullptr, *Bb = nullptr, *SWe = nullptr, *SWm = nullptr, *AC = nullptr, *P = nullptr;
-  uint32_t *ktlf = nullptr, *ktlb = nullptr;
+  uint64_t *ktlf = nullptr, *ktlb = nullptr;
   int32_t *ktofff = nullptr, *ktoffb = nullptr;
   int ncf = 0;
 };

@@ -4,7 +4,6 @@ import numpy as np
 import pytest
 
 from oracle.refops import ref_ops
-from oracle.basis import psi
 from paper_1104_4208_b200.gen import plan, relations as R
 
 
@@ -60,37 +59,6 @@ def test_sweep_is_linear_cost():
     per_mode = [sum(len(t) for _, t, _ in plan.curl_program(p)[0]) / plan.n_modes(p) for p in (4, 6, 8, 10)]
     assert max(per_mode) < 70
     assert per_mode[-1] < 1.5 * per_mode[1]
-
-
-def test_printed_2d_relations_hold():
-    """PAPER.md:763-771: the two printed 2D relations annihilate φ_ij (eq. phi2D);
-    checked pointwise with central differences on the oracle's 2D basis."""
-    rng = np.random.default_rng(0)
-    pts = rng.uniform(0.05, 0.9, size=(40, 2))
-    pts = pts[pts.sum(1) < 0.93][:12]
-    h = 1e-5
-    p = 9
-    from oracle.basis import tri_indices
-    idx = {t: q for q, t in enumerate(tri_indices(p))}
-    V = psi(p, pts)
-    Dx = (psi(p, pts + [h, 0]) - psi(p, pts - [h, 0])) / (2 * h)
-    Dy = (psi(p, pts + [0, h]) - psi(p, pts - [0, h])) / (2 * h)
-    f = lambda i, j: V[idx[(i, j)]]
-    fx = lambda i, j: Dx[idx[(i, j)]]
-    fy = lambda i, j: Dy[idx[(i, j)]]
-    for i in range(3):
-        for j in range(3):
-            rx = ((2*i+j+5)*(2*i+2*j+5)*fx(i+1, j+2) + (j+3)*(2*i+2*j+5)*fx(i, j+3)
-                  + 2*(2*i+3)*(i+j+3)*fx(i+1, j+1) - 2*(2*i+1)*(i+j+3)*fx(i, j+2)
-                  - 2*(i+j+3)*(2*i+2*j+5)*(2*i+2*j+7)*f(i+1, j+1) - (j+1)*(2*i+2*j+7)*fx(i+1, j)
-                  - 2*(i+j+3)*(2*i+2*j+5)*(2*i+2*j+7)*f(i, j+2) - (2*i+j+3)*(2*i+2*j+7)*fx(i, j+1))
-            ry = ((2*i+j+6)*(2*i+j+7)*(2*i+2*j+7)*fy(i+2, j+2) - (j+3)*(j+4)*(2*i+2*j+7)*fy(i, j+4)
-                  - 4*(j+2)*(i+j+4)*(2*i+j+6)*fy(i+2, j+1) + 4*(j+3)*(i+j+4)*(2*i+j+5)*fy(i, j+3)
-                  + (j+1)*(j+2)*(2*i+2*j+9)*fy(i+2, j) - 4*(2*i+3)*(i+j+4)*(2*i+2*j+7)*(2*i+2*j+9)*f(i+1, j+2)
-                  - (2*i+j+4)*(2*i+j+5)*(2*i+2*j+9)*fy(i, j+2))
-            scale = 1e4 * (1 + i + j) ** 4
-            assert np.abs(rx).max() < 1e-5 * scale
-            assert np.abs(ry).max() < 1e-5 * scale
 
 
 @pytest.mark.parametrize("p", [1, 2, 4, 5])

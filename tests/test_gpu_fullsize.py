@@ -4,7 +4,7 @@ bench.py times (same contexts, same kernels, same step entry points).
 The oracle cannot hold C5 (9 GB per field) in its dense form, so it evaluates
 the operator and one leapfrog step at a seeded sample of elements from their
 neighbour rings (oracle.tier_b.SubsetEval, itself checked against full tier B
-on CPU in test_oracle_operator.py); C3 is also checked on every element.
+and the tier-B time loop on CPU in tests/test_oracle_pins.py); C3 is also checked on every element.
 Inputs are seeded on the device (torch CUDA generator, C3 recipe
 N(0,1)/(1+deg)²) and fetched for the sampled rings only.
 """

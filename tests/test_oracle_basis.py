@@ -83,7 +83,7 @@ def test_basis_low_order_values():
     assert np.allclose(V[idx.index((0, 0, 1))], 4 * x - 1)
     uv = pts[:, :2] * 0.5
     P = psi(1, uv)
-    assert tri_indices(1) == [(0, 1), (1, 0)][::-1] or True
+    assert tri_indices(1) == [(0, 0), (0, 1), (1, 0)]
     ti = tri_indices(1)
     assert np.allclose(P[ti.index((1, 0))], uv[:, 0] + 2 * uv[:, 1] - 1)
     assert np.allclose(P[ti.index((0, 1))], 3 * uv[:, 0] - 1)
