@@ -5,10 +5,16 @@ H-stage + one E-stage over the whole mesh) on B200.
 python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 Metric (BASELINE.json): DOF-updates/s per DG time step (FP64) = 6·N·n_tet / step
-time, whole job over all ranks.  Default workload = configs[1] (C2: 16³ Kuhn
-periodic, 24,576 tets, p=4, central flux).  Inputs are resident in HBM when the
-timed region starts; L2 (126 MB) is flushed between timed steps (a 512 MiB
-write), each step is timed with CUDA events on the library's stream.
+time, whole job over all ranks.  BASELINE.json's metric names no config, so the
+default workload is the largest single-GPU config, configs[4] (C5: 48³ Kuhn
+periodic, 663,552 tets, p=10, 1.14e9 DOFs, central flux); --config picks another
+(C1-C4 are parity cases).  Inputs are resident in HBM when the timed region
+starts; with a state larger than 2x L2 (C3-C5) no flush is needed, otherwise L2
+(126 MB) is flushed between timed steps (a 512 MiB write); each step is timed
+with CUDA events on the library's stream.
+roofline: both roofs are reported, HBM (algorithmic bytes) and
+FP64 (algorithmic flops of the paper's O(N) operator); `bound`
+names the larger fraction.
 `e2e` times the same steps through dgm_step_host (pinned host → device copy of
 E,H, the step, device → host copy of E,H, every step).
 Multi-GPU: the path does not shard in this build (north_star: one GPU), so N>1
@@ -42,7 +48,7 @@ def parse():
                     help="timed steps (default: enough for ~0.25 s of GPU time, so the clock sampler "
                          "sees the timed region; 3 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=list(di.CONFIGS))
+    ap.add_argument("--config", default="C5", choices=list(di.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -140,6 +146,54 @@ def algorithmic_bytes_per_stage(n_tet, N, upwind):
     return n_tet * (9 * N * 8 + meta)
 
 
+# SURVEY.md §8(d) "Algorithmic flops" per element per step, counted from the
+# generated tables (not measured): 4 × [sweeps + 15N + 32·N_F + 4·T], 4 = 2 stages ×
+# 2 flops/FMA, sweeps = curl sweep FMAs per field (App. A.3), T = the realistic
+# trace cost of one scalar component over the 4 faces (min(dense-sparse, Horner)).
+SWEEP_FMA = {2: 88, 4: 920, 6: 3366, 8: 8252, 10: 16410}
+TRACE_T = {2: 114, 4: 812, 6: 2240, 8: 4410, 10: 7656}
+
+
+def algorithmic_flops_per_stage(n_tet, p):
+    N = (p + 1) * (p + 2) * (p + 3) // 6
+    NF = (p + 1) * (p + 2) // 2
+    return n_tet * 2 * (SWEEP_FMA[p] + 15 * N + 32 * NF + 4 * TRACE_T[p])
+
+
+def fp64_peak():
+    """Measured FP64 peaks on this pool (tools/peaks/fp64_peaks.cu, newest profiles/rNN file):
+    the DMMA (m8n8k4 tensor) figure, the higher of DMMA and DFMA."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp64_peaks.txt")), reverse=True):
+        best = {}
+        with open(path) as f:
+            for ln in f:
+                try:
+                    d = json.loads(ln)
+                except ValueError:
+                    continue
+                if "tflops" in d:
+                    best[d["kind"]] = max(best.get(d["kind"], 0.0), d["tflops"])
+        if best:
+            k = max(best, key=best.get)
+            return best[k], f"{os.path.relpath(path, ROOT)} ({k}, {best[k]:.2f} TFLOP/s)"
+    return 37.0, "nominal B200 FP64 (no measured file)"
+
+
+def stage_kernels(engine, p):
+    """Kernel names of one stage (ncu launch-list names) for the roofline line."""
+    if engine == "dense":
+        return ["dense_flux_kernel", "gemm_kernel<stage>", "gemm_kernel<trace>"]
+    return ["lane_stage_kernel" if p <= 6 else "stream_kernel"]
+
+
+def config_dict(name, cfg, n_tet, N, world=1):
+    """The workload description, identical for both arms (same keys and values)."""
+    return {"workload": name, "n_tet": int(n_tet), "p": cfg["p"], "N": int(N), "flux": cfg["flux"],
+            "periodic": list(cfg["periodic"]), "parallelism": "replicas only" if world > 1 else "single GPU",
+            "fields": "seeded random coefficients (C3 recipe); timing is data independent"}
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_1104_4208_b200 import Context
@@ -210,33 +264,46 @@ def run_ours(args, rank, world):
                    f"state {state_bytes / 1e9:.2f} GB > 2x L2: no flush"))
     # roofline of the operator application per stage.  With DGM_STEP_CONTINUE a step
     # is two stages: sparse = one stage kernel each; dense = flux + stage GEMM + trace
-    # GEMM each (the "launch" below is then the whole stage, timed as step/2)
+    # GEMM each.  The "launch" below is the whole stage (all its kernels), timed on the
+    # library's stream as step/2; roofline.kernel names them.
     upwind = cfg["flux"] == "upwind"
     per_launch_s = (t_total / args.steps) / 2
     B = algorithmic_bytes_per_stage(n, N, upwind)
+    Fl = algorithmic_flops_per_stage(n, p)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
+    f64, f64_src = fp64_peak()
     engine = ctx.engine
-    if engine == "dense":
-        kern = f"dense stage<{p}> (dense_flux_kernel + gemm_kernel<stage> + gemm_kernel<trace>)"
-    else:
-        kern = f"{'lane_stage_kernel' if p <= 6 else 'stream_kernel'}<{p}>"
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tpath):
+    kerns = stage_kernels(engine, p)
+    traffic, tsrc = None, None
+    import glob
+    for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         with open(tpath) as f:
             tj = json.load(f)
-        for tr in (tj.get(args.config), tj.get(args.config + "_dense")):
-            if tr and tr.get("kernel") == kern:
-                traffic = tr["dram_bytes_per_launch"]
+        tr = tj.get(f"{args.config}_{engine}")
+        if tr and tr.get("kernels") == kerns:
+            traffic = tr["dram_bytes_per_stage"]
+            tsrc = f"{os.path.relpath(tpath, ROOT)} (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum, summed over the stage's kernels)"
+            break
+    ach_b = B / per_launch_s / 1e9
+    ach_f = Fl / per_launch_s / 1e12
+    hfrac, ffrac = ach_b / hbm, ach_f / f64
+    bound = "hbm" if hfrac >= ffrac else "fp64"
     res["engine"] = engine
-    res["roofline"] = {"bound": "hbm", "achieved": B / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
-                       "frac": (B / per_launch_s / 1e9) / hbm, "traffic": traffic,
-                       "traffic_source": "profiles/r01_traffic.json (ncu dram__bytes_read+write per launch; dense: per stage)"
-                       if traffic is not None else None,
-                       "kernel": kern, "bytes_per_launch": B, "launch_ms": per_launch_s * 1e3,
-                       "launches_per_step": launches / args.steps,
-                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk else "fallback 6.65 TB/s"}
+    res["roofline"] = {"bound": bound,
+                       "achieved": ach_b if bound == "hbm" else ach_f, "peak": hbm if bound == "hbm" else f64,
+                       "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": max(hfrac, ffrac),
+                       "traffic": traffic, "traffic_source": tsrc,
+                       "hbm": {"achieved": ach_b, "peak": hbm, "unit": "GB/s", "frac": hfrac,
+                               "bytes_per_stage": B,
+                               "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk
+                               else "fallback 6.65 TB/s"},
+                       "fp64": {"achieved": ach_f, "peak": f64, "unit": "TFLOP/s", "frac": ffrac,
+                                "flops_per_stage": Fl, "peak_source": f64_src,
+                                "flops_definition": "SURVEY.md §8(d): 2 × (curl sweeps + 15N + 32 N_F + 4T) per element-stage"},
+                       "fp64_frac": ffrac, "hbm_frac": hfrac,
+                       "kernel": " + ".join(f"{k}<{p}>" for k in kerns), "kernels": kerns,
+                       "launch_ms": per_launch_s * 1e3, "launches_per_step": launches / args.steps}
     # e2e through the C ABI with HOST buffers: H2D of E,H, the step, D2H of E,H
     if not args.no_e2e:
         Eh = torch.empty((3, n, ctx.ld), dtype=torch.float64).pin_memory()
@@ -263,6 +330,7 @@ def run_ours(args, rank, world):
         res["e2e"] = {"value": world * dof * args.steps / te, "unit": "DOF-updates/s",
                       "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
                       "api": "dgm_step_host (C ABI, pinned host E,H; entry traces recomputed each call)"}
+    res["_E"], res["_H"] = E, H
     return res, cfg
 
 
@@ -283,33 +351,76 @@ def dist_max(x, world):
     return float(t.item())
 
 
-def cpu_baseline(cfg_name, budget_s=20.0, max_steps=1000):
-    """The oracle (tier B, NumPy/BLAS FP64) timed on the host on a bounded sample:
-    as many full symplectic-Euler steps of the same config as fit in ~budget_s."""
+def oracle_setup(cfg_name, E=None, H=None):
+    """The oracle (tier B) for a config, with the bench's seeded fields."""
     import oracle.tier_b as tb
-    cfg, m, eps, mu, rep, E, H = make_problem(cfg_name)
-    p = cfg["p"]
+    cfg = di.CONFIGS[cfg_name]
+    m = di.config_mesh(cfg_name)
+    eps, mu = di.config_materials(cfg_name, m.n_tet)
+    rep = m.rep if any(cfg["periodic"]) else None
+    if E is None:
+        _, _, _, _, _, E, H = make_problem(cfg_name)
     t0 = time.perf_counter()
-    B = tb.TierB(m.xyz, m.tet, rep, p, eps, mu, cfg["flux"])
-    setup = time.perf_counter() - t0
-    dt = 1e-4
-    # warm-up step (excluded)
-    H = H + dt * B.dH(E, H)
-    E = E + dt * B.dE(E, H)
-    steps = 0
+    B = tb.TierB(m.xyz, m.tet, rep, cfg["p"], eps, mu, cfg["flux"])
+    return cfg, m, B, tb.SubsetEval(B), E, H, time.perf_counter() - t0
+
+
+CHUNK = 4096   # elements per oracle sample (a contiguous run of the mesh's element order)
+
+
+def oracle_chunk(S, E, H, k, n_tet, dt=1e-4):
+    """One bounded sample of the workload on the oracle: a full symplectic-Euler step
+    (H on the 1-ring, then E) evaluated by oracle.tier_b.SubsetEval
+    at CHUNK contiguous elements (chunk k, wrapping).  Returns the element count."""
+    e0 = (k * CHUNK) % max(1, n_tet)
+    el = np.arange(e0, min(n_tet, e0 + CHUNK))
+    S.step(lambda idx: (E[:, idx], H[:, idx]), el, dt)
+    return el.size
+
+
+def cpu_baseline(cfg_name, budget_s=20.0, E=None, H=None):
+    """The oracle (tier B) timed on the host on a bounded sample of the same workload:
+    as many CHUNK-element symplectic-Euler steps (SubsetEval) as fit in ~budget_s."""
+    cfg, m, B, S, E, H, setup = oracle_setup(cfg_name, E, H)
+    oracle_chunk(S, E, H, 0, m.n_tet)      # warm-up (excluded)
+    done = chunks = 0
     t0 = time.perf_counter()
     while True:
-        H = H + dt * B.dH(E, H)
-        E = E + dt * B.dE(E, H)
-        steps += 1
+        done += oracle_chunk(S, E, H, 1 + chunks, m.n_tet)
+        chunks += 1
         el = time.perf_counter() - t0
-        if el > budget_s or steps >= max_steps:
+        if el > budget_s:
             break
     cores = len(os.sched_getaffinity(0))
-    N = B.N
-    return {"value": 6.0 * N * m.n_tet * steps / el, "unit": "DOF-updates/s", "cores": cores, "kind": "oracle",
-            "sample": f"{steps} full symplectic-Euler steps of {cfg_name} ({m.n_tet} tets, p={p}) with oracle tier B "
-                      f"(NumPy+OpenBLAS FP64, {cores} host threads), {el:.1f} s, setup {setup:.1f} s excluded"}
+    return {"value": 6.0 * B.N * done / el, "unit": "DOF-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"{chunks} symplectic-Euler steps of {cfg_name} ({m.n_tet} tets, p={cfg['p']}), each on "
+                      f"{CHUNK} contiguous elements (oracle tier B via SubsetEval: H on the 1-ring, then E), "
+                      f"{done} element-steps in {el:.1f} s, NumPy+BLAS FP64, {cores} host threads; "
+                      f"setup {setup:.1f} s excluded"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands (tier B via SubsetEval) on the host,
+    W warm-up samples then K timed samples of the same workload (CHUNK elements each)."""
+    cfg, m, B, S, E, H, setup = oracle_setup(args.config)
+    for k in range(args.warmup):
+        oracle_chunk(S, E, H, k, m.n_tet)
+    done = 0
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        done += oracle_chunk(S, E, H, args.warmup + k, m.n_tet)
+    el = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    value = 6.0 * B.N * done / el
+    sample = (f"{args.steps} timed symplectic-Euler steps (after {args.warmup} warm-up) of {args.config}, each on "
+              f"{CHUNK} contiguous elements (oracle tier B via SubsetEval), {done} element-steps in {el:.1f} s, "
+              f"{cores} host threads; setup {setup:.1f} s excluded")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args.config, cfg, m.n_tet, B.N),
+            "cpu_baseline": {"kind": "oracle", "cores": cores, "sample": sample, "value": value},
+            "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -321,16 +432,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        cb = cpu_baseline(args.config, budget_s=max(5.0, min(60.0, 3.0 * args.steps)))
-        cfg = di.CONFIGS[args.config]
-        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "DOF-updates/s", "n_gpus": 0,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.config, "n_tet": int(np.prod(cfg["n"])) * 6, "p": cfg["p"],
-                           "flux": cfg["flux"]},
-                "cpu_baseline": {k: cb[k] for k in ("kind", "cores", "sample")} | {"value": cb["value"]},
-                "e2e": {"value": cb["value"], "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        print(json.dumps(run_reference(args)))
         return 0
     if world > 1:
         import torch
@@ -343,16 +445,13 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": args.config, "n_tet": res["n_tet"], "p": cfg["p"], "N": res["N"],
-                           "flux": cfg["flux"], "periodic": cfg["periodic"], "l2": res["l2"],
-                           "engine": res["engine"],
-                           "parallelism": "replicas only" if world > 1 else "single GPU",
-                           "fields": "seeded random coefficients (C3 recipe); timing is data independent"},
+                "config": config_dict(args.config, cfg, res["n_tet"], res["N"], world=world),
+                "engine": res["engine"], "l2": res["l2"],
                 "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["launches"]}
         if "e2e" in res:
             line["e2e"] = res["e2e"]
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args.config)
+            line["cpu_baseline"] = cpu_baseline(args.config, E=res.pop("_E"), H=res.pop("_H"))
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

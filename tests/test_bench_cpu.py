@@ -51,3 +51,25 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["config"]["workload"] == "C1"
+    assert line["steps"] == 2 and "2 timed" in line["cpu_baseline"]["sample"]
+    # the same config dict as our arm's line (the driver compares them)
+    sys.path.insert(0, ROOT)
+    import bench
+    import dgm_inputs as di
+    cfg = di.CONFIGS["C1"]
+    assert line["config"] == bench.config_dict("C1", cfg, 384, 10)
+
+
+def test_algorithmic_counts():
+    """SURVEY.md §8(d) per-unit figures used for the FP64 roof: the curl sweep FMAs
+    per field equal twice the generated relation coefficients of ∂x, ∂y, ∂z (within
+    the pivot bookkeeping), and the flops scale as O(N) per element."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1104_4208_b200.gen import plan
+    for p in (4, 6, 8, 10):
+        rels, _ = plan.load(p)
+        terms = 2 * sum(len(t) for d in range(3) for t in rels[d].values())
+        assert abs(terms - bench.SWEEP_FMA[p]) <= 0.05 * bench.SWEEP_FMA[p], (p, terms)
+    per_dof = [bench.algorithmic_flops_per_stage(1, p) / ((p + 1) * (p + 2) * (p + 3) // 6) for p in (4, 6, 8, 10)]
+    assert max(per_dof) < 2 * min(per_dof)
