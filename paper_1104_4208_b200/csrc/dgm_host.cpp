@@ -482,8 +482,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   size_t bytes = 0;
   for (int v = 0; v < nvar; ++v) {
-    bytes += al(P1[v].size() * 8) + al(P2[v].size() * 8) + al(l2[v].size() * 4 + 4) + al(o2[v].size() * 4);
-    for (int i = 1; i < 4; ++i) bytes += al(l1[v][i].size() * 4 + 4) + al(o1[v][i].size() * 4);
+    bytes += al(P1[v].size() * 8) + al(P2[v].size() * 8) + al(l2[v].size() * 8 + 4) + al(o2[v].size() * 4 + 4);
+    for (int i = 1; i < 4; ++i) bytes += al(l1[v][i].size() * 8 + 4) + al(o1[v][i].size() * 4 + 4);
   }
   CUDA_TRY(c, cudaMalloc(&c->d_dense, bytes));
   char *base = (char *)c->d_dense;

@@ -41,8 +41,11 @@ def _case(p, periodic, n, seed=3):
 CASES = [((False,) * 3, 2), ((True,) * 3, 3), ((False, True, True), (2, 3, 3))]
 
 
-@pytest.mark.parametrize("periodic,n", CASES)
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 6, 8])
+VARMAT_CASES = [(p, pc, n) for p in (1, 2, 3, 4, 6, 8) for pc, n in CASES] + \
+    [(9, (False,) * 3, 2), (10, (False,) * 3, 2), (10, (True,) * 3, 3)]   # > 256 k-tiles of the point GEMM
+
+
+@pytest.mark.parametrize("p,periodic,n", VARMAT_CASES)
 def test_varmat_apply_parity(p, periodic, n):
     m, rep, c, V = _case(p, periodic, n)
     rng = np.random.default_rng(p)
