@@ -184,6 +184,8 @@ def stage_kernels(engine, p):
     """Kernel names of one stage (ncu launch-list names) for the roofline line."""
     if engine == "dense":
         return ["dense_flux_kernel", "gemm_kernel<stage>", "gemm_kernel<trace>"]
+    if engine == "hybrid":
+        return ["dense_flux_kernel", "curl_kernel", "gemm_kernel<stage>", "gemm_kernel<trace>"]
     return ["lane_stage_kernel" if p <= 6 else "stream_kernel"]
 
 

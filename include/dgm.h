@@ -77,7 +77,7 @@ typedef struct {
   const int32_t *rep;   /* [n_vert] host, periodic representative; NULL = id  */
 } dgm_mesh;
 
-/* Execution engine of the stage kernels.  Both compute the same operator (same
+/* Execution engine of the stage kernels.  All compute the same operator (same
  * flux, traces, lift, update; parity-tested against the oracle); they differ in how
  * the reference-frame operators are applied:
  *   SPARSE: the paper's recurrence sweeps and sum-factorised traces/lifts
@@ -86,13 +86,18 @@ typedef struct {
  *   DENSE:  the same operators assembled once per context into matrices (from the
  *           exact programs) and applied as block-sparse FP64 tensor-core GEMMs over
  *           tiles of elements (mma.sync m8n8k4), 3 launches per stage.
- *   AUTO:   SPARSE for p <= 5, DENSE for p >= 6 (measured faster there).
- * The environment variable DGM_ENGINE=sparse|dense overrides AUTO.  For measurements,
+ *   HYBRID: (orders 7..10) the curl by the paper's recurrences as streamed
+ *           lane-per-element sweeps on the FP64 pipes, written to an
+ *           internal ĉ buffer and added in the epilogue of the DENSE stage GEMM, which
+ *           then applies only the lift; traces as in DENSE.  4 launches per stage.
+ *   AUTO:   SPARSE for p <= 5, DENSE for p >= 6 (measured fastest there; HYBRID ties
+ *           DENSE at p = 8 and is 2% slower at p = 10).  Mixed orders use DENSE.
+ * The environment variable DGM_ENGINE=sparse|dense|hybrid overrides AUTO.  For measurements,
  * DGM_STAGE_NH / DGM_TRACE_NH = 1|2 force the dense GEMM tile width (one or two 96-column
  * warp columns; default one) and DGM_TILE_ORDER=0 the static GEMM tile order
  * (default: dynamic, from a per-context self-resetting counter, so one context must not run dense GEMMs
  * on two streams at once); results are the same operator. */
-typedef enum { DGM_ENGINE_AUTO = 0, DGM_ENGINE_SPARSE = 1, DGM_ENGINE_DENSE = 2 } dgm_engine_kind;
+typedef enum { DGM_ENGINE_AUTO = 0, DGM_ENGINE_SPARSE = 1, DGM_ENGINE_DENSE = 2, DGM_ENGINE_HYBRID = 3 } dgm_engine_kind;
 
 typedef struct {
   int32_t flux;          /* dgm_flux                                          */
@@ -235,7 +240,7 @@ int64_t dgm_last_launches(const dgm_ctx *ctx);
  * NULL).  Point i of element T is X0_T + F_T ξ_i. */
 dgm_status dgm_quadrature_host(int order, int64_t *Q, double *xi, double *w);
 
-/* The engine the context resolved to (DGM_ENGINE_SPARSE or DGM_ENGINE_DENSE). */
+/* The engine the context resolved to (DGM_ENGINE_SPARSE, _DENSE or _HYBRID). */
 int dgm_engine(const dgm_ctx *ctx);
 
 const char *dgm_last_error(const dgm_ctx *ctx);

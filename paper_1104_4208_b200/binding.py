@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libdgm.so")
 DGM_OK, DGM_EINVAL, DGM_EMESH, DGM_EORDER, DGM_ECUDA, DGM_ENOMEM = range(6)
 STATUS = {0: "DGM_OK", 1: "DGM_EINVAL", 2: "DGM_EMESH", 3: "DGM_EORDER", 4: "DGM_ECUDA", 5: "DGM_ENOMEM"}
 FLUX = {"central": 0, "upwind": 1, "stabilized": 2}
-ENGINE = {"auto": 0, "sparse": 1, "dense": 2}
+ENGINE = {"auto": 0, "sparse": 1, "dense": 2, "hybrid": 3}
 DGM_STEP_CONTINUE = 1
 EXPORTS = ["dgm_create", "dgm_layout", "dgm_apply_curl", "dgm_apply_flux", "dgm_step", "dgm_step_ex", "dgm_step_host",
            "dgm_energy", "dgm_spectral_radius", "dgm_faces", "dgm_step_sc", "dgm_rhs_sc", "dgm_energy_sc", "dgm_tables", "dgm_match_faces_host", "dgm_last_launches", "dgm_engine", "dgm_quadrature_host", "dgm_last_error", "dgm_destroy"]
@@ -299,8 +299,8 @@ class Context:
 
     @property
     def engine(self):
-        """'sparse' or 'dense': the engine this context resolved to (dgm_engine)."""
-        return {1: "sparse", 2: "dense"}[self._lib.dgm_engine(self.h)]
+        """'sparse', 'dense' or 'hybrid': the engine this context resolved to (dgm_engine)."""
+        return {1: "sparse", 2: "dense", 3: "hybrid"}[self._lib.dgm_engine(self.h)]
 
     def dgm_last_launches(self):
         return int(self._lib.dgm_last_launches(self.h))

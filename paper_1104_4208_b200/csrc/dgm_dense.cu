@@ -93,6 +93,11 @@ struct GemmArgs {
   int rawld, rawNk;
   int unit_m;
   unsigned long long *tile_ctr;   // dynamic tile counter [claims, arrivals] (self-resetting), or null: static order
+  // EPI_STAGE, hybrid engine: the curl ĉ from the streamed sweeps is added to the
+  // accumulator, ĉ[c][e][b] at cc + c*ccs + e*ldc + b for b < ncc (else 0)
+  const double *cc;
+  int64_t ccs;
+  int ldc, ncc;
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
       double *out = upd ? g.X : g.dX;
       for (int base = tid; base < BM * MODES; base += U * NTHREADS) {
         int64_t o[U];
-        double xv[U][3];
+        double xv[U][3], cv[U][3];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int idx = base + u * NTHREADS;
@@ -358,6 +363,9 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
 #pragma unroll
           for (int cc = 0; cc < 3; ++cc)
             xv[u][cc] = (o[u] >= 0 && g.out_mode != OUT_WRITE && !g.raw) ? out[cc * cs + o[u]] : 0.0;
+          const bool hc = g.cc && o[u] >= 0 && b < g.ncc;
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) cv[u][cc] = hc ? g.cc[cc * g.ccs + e * g.ldc + b] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const double cm = G[6];
           // tile mode ml -> warp column h = (ml/8) % NH, its mode ((ml/8)/NH) 8 + ml%8
           const int hb = ((ml >> 3) % NH) * BN + ((ml >> 3) / NH) * 8 + (ml & 7);
-          const double v0 = Cs[r][hb], v1 = Cs[r][32 + hb], v2 = Cs[r][64 + hb];
+          const double v0 = Cs[r][hb] + cv[u][0], v1 = Cs[r][32 + hb] + cv[u][1], v2 = Cs[r][64 + hb] + cv[u][2];
           if (g.raw) {   // residual before the (variable-material) inverse mass
             double *rw = g.raw + (m0 + r) * (int64_t)g.rawld + 32 * NH * nt + ml;
             rw[0] = v0;
@@ -551,8 +559,19 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   g.nkt = D.nkt1;
   g.NC = D.nc1;
   g.Np = D.nc1 / 3;
-  // curl only / flux only: restrict the k-tile lists
-  const int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
+  // curl only / flux only: restrict the k-tile lists.  Hybrid engine: the curl comes
+  // from the streamed recurrence sweeps (ĉ, added in the epilogue), the GEMM does the
+  // lift only
+  int sel = (a.do_curl ? 1 : 0) | (a.do_flux ? 2 : 0);
+  if (c->sparse_curl && a.do_curl) {
+    dgm_status s = launch_curl(c, a.Y, D.Cc, st);
+    if (s != DGM_OK) return s;
+    sel &= 2;
+    g.cc = D.Cc;
+    g.ccs = c->n_tet * (int64_t)D.ldc;
+    g.ldc = D.ldc;
+    g.ncc = c->p * (c->p + 1) * (c->p + 2) / 6;
+  }
   g.ktl = D.ktl1[v][sel];
   g.ktoff = D.ktoff1[v][sel];
   g.ntiles_n = D.nc1 / 3 / (32 * D.stage_nh);
@@ -600,6 +619,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     if ((s = gemm_go<EPI_TRACE>(c, f, st)) != DGM_OK) return s;
     GemmArgs b = g;
     b.raw = nullptr;
+    b.cc = nullptr;   // ĉ entered the residual already
     b.p0 = b.p1 = D.P;
     b.ld0 = b.ld1 = 3 * Qk;
     b.cs = Qk;
@@ -619,6 +639,16 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   }
   if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st, v);
   return DGM_OK;
+}
+
+dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st) {
+  switch (c->p) {
+    case 7: return launch_curl_p7(c, Y, C, st);
+    case 8: return launch_curl_p8(c, Y, C, st);
+    case 9: return launch_curl_p9(c, Y, C, st);
+    case 10: return launch_curl_p10(c, Y, C, st);
+  }
+  return set_err(c, DGM_EORDER, "streamed curl sweeps: orders 7..10");
 }
 
 dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field) {

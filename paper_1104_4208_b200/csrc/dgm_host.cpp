@@ -450,6 +450,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   std::vector<uint64_t> l1[2][4], l2[2];
   std::vector<int32_t> o1[2][4], o2[2];
   for (int v = 0; v < nvar; ++v) {
+    tiles(B1v[v], nc1, Np / (32 * NH), true, 0, 0, l1[v][0], o1[v][0]);   // none (sparse curl only)
     tiles(B1v[v], nc1, Np / (32 * NH), true, 0, k1a, l1[v][1], o1[v][1]);
     tiles(B1v[v], nc1, Np / (32 * NH), true, k1a, K1, l1[v][2], o1[v][2]);
     tiles(B1v[v], nc1, Np / (32 * NH), true, 0, K1, l1[v][3], o1[v][3]);
@@ -467,8 +468,8 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     for (size_t t = 0; t + 1 < o2[0].size(); ++t) {
       long w0 = 0, w1 = 0;
       for (int i = o2[0][t]; i < o2[0][t + 1]; ++i) {
-        w0 += __builtin_popcount((l2[0][i] >> 8) & 0xFFFu);
-        w1 += __builtin_popcount((l2[0][i] >> 20) & 0xFFFu);
+        w0 += __builtin_popcountll((l2[0][i] >> 16) & 0xFFFu);
+        w1 += __builtin_popcountll((l2[0][i] >> 28) & 0xFFFu);
       }
       std::fprintf(stderr, "  B2 n-tile %zu: %d k-tiles, blocks %ld | %ld\n", t, o2[0][t + 1] - o2[0][t], w0, w1);
     }
@@ -483,7 +484,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   size_t bytes = 0;
   for (int v = 0; v < nvar; ++v) {
     bytes += al(P1[v].size() * 8) + al(P2[v].size() * 8) + al(l2[v].size() * 8 + 4) + al(o2[v].size() * 4 + 4);
-    for (int i = 1; i < 4; ++i) bytes += al(l1[v][i].size() * 8 + 4) + al(o1[v][i].size() * 4 + 4);
+    for (int i = 0; i < 4; ++i) bytes += al(l1[v][i].size() * 8 + 4) + al(o1[v][i].size() * 4 + 4);
   }
   CUDA_TRY(c, cudaMalloc(&c->d_dense, bytes));
   char *base = (char *)c->d_dense;
@@ -499,7 +500,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   for (int v = 0; v < nvar; ++v) {
     D.B1[v] = (double *)put(P1[v].data(), P1[v].size() * 8);
     D.B2[v] = (double *)put(P2[v].data(), P2[v].size() * 8);
-    for (int i = 1; i < 4; ++i) {
+    for (int i = 0; i < 4; ++i) {
       D.ktl1[v][i] = (uint64_t *)put(l1[v][i].data(), l1[v][i].size() * 8);
       D.ktoff1[v][i] = (int32_t *)put(o1[v][i].data(), o1[v][i].size() * 4);
     }
@@ -510,7 +511,7 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
   if (nvar == 1) {   // equal orders: both fields use the same operators
     D.B1[1] = D.B1[0];
     D.B2[1] = D.B2[0];
-    for (int i = 1; i < 4; ++i) {
+    for (int i = 0; i < 4; ++i) {
       D.ktl1[1][i] = D.ktl1[0][i];
       D.ktoff1[1][i] = D.ktoff1[0][i];
     }
@@ -562,6 +563,10 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
     CUDA_TRY(c, cudaMalloc(&D.P, sizeof(double) * 3 * (size_t)Qk * (size_t)(n_or1(c))));
   }
   CUDA_TRY(c, cudaMalloc(&D.AB, sizeof(double) * 8 * (size_t)NFk * (size_t)(c->n_tet > 0 ? c->n_tet : 1)));
+  if (c->sparse_curl) {   // ĉ scratch of the streamed curl sweeps, rows of whole 16-mode chunks
+    D.ldc = (c->p * (c->p + 1) * (c->p + 2) / 6 + 15) / 16 * 16;
+    CUDA_TRY(c, cudaMalloc(&D.Cc, sizeof(double) * 3 * (size_t)D.ldc * (size_t)c->n_tet));
+  }
   if (!(std::getenv("DGM_TILE_ORDER") && std::atoi(std::getenv("DGM_TILE_ORDER")) == 0))   // 0: static order
   {
     CUDA_TRY(c, cudaMalloc(&D.tile_ctr, 64));
@@ -579,6 +584,7 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->d_dense);
   cudaFree(c->dense.AB);
   cudaFree(c->dense.tile_ctr);
+  cudaFree(c->dense.Cc);
   for (void *q : {(void *)c->dense.Bf, (void *)c->dense.Bb, (void *)c->dense.ktlf, (void *)c->dense.ktofff,
                   (void *)c->dense.ktlb, (void *)c->dense.ktoffb, (void *)c->dense.SWe, (void *)c->dense.SWm,
                   (void *)c->dense.AC, (void *)c->dense.P})
@@ -613,7 +619,7 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
   dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0, 0};
-  if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_DENSE) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
+  if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_HYBRID) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
   if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
     return dgm::set_err(c, DGM_EINVAL, "unknown flux");
   const int p = order;
@@ -624,16 +630,29 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   c->LD = (c->N + 3) & ~3;
   c->n_tet = n;
   c->flux = o.flux;
-  // engine: explicit option, else DGM_ENGINE, else by order (dense measured faster for p >= 6)
-  c->engine = o.engine == DGM_ENGINE_DENSE ? 1 : o.engine == DGM_ENGINE_SPARSE ? 0 : (p >= 6 ? 1 : 0);
-  if (o.engine == DGM_ENGINE_AUTO)
-    if (const char *v = std::getenv("DGM_ENGINE")) c->engine = std::strcmp(v, "dense") == 0 ? 1 : 0;
+  // engine: explicit option, else DGM_ENGINE, else by order (measured): the
+  // sparse recurrence kernels for p <= 5, dense DMMA contractions for p >= 6 (the hybrid,
+  // streamed recurrence curl + DMMA lift and traces, ties at p = 8 and loses 2% at p = 10)
+  int kind = o.engine;
+  if (kind == DGM_ENGINE_AUTO) {
+    kind = p >= 6 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE;
+    if (const char *v = std::getenv("DGM_ENGINE"))
+      kind = std::strcmp(v, "dense") == 0 ? DGM_ENGINE_DENSE
+             : std::strcmp(v, "hybrid") == 0 && p >= dgm::kCurlPmin ? DGM_ENGINE_HYBRID
+                                                                     : DGM_ENGINE_SPARSE;
+  }
+  if (kind == DGM_ENGINE_HYBRID && (p < dgm::kCurlPmin || p > dgm::kCurlPmax))
+    return dgm::set_err(c, DGM_EINVAL, "the hybrid engine covers orders 7..10");
+  c->engine = kind == DGM_ENGINE_SPARSE ? 0 : 1;
+  c->sparse_curl = kind == DGM_ENGINE_HYBRID ? 1 : 0;
   // mixed orders E ∈ P^p, H ∈ P^{p-1}: dense engine, central/upwind
   if (o.mixed_order) {
     if (p < 2) return dgm::set_err(c, DGM_EORDER, "mixed orders need order >= 2");
     if (o.flux == DGM_FLUX_STABILIZED) return dgm::set_err(c, DGM_EINVAL, "mixed orders: central or upwind flux only");
-    if (o.engine == DGM_ENGINE_SPARSE) return dgm::set_err(c, DGM_EINVAL, "mixed orders need the dense engine");
+    if (o.engine == DGM_ENGINE_SPARSE || o.engine == DGM_ENGINE_HYBRID)
+      return dgm::set_err(c, DGM_EINVAL, "mixed orders need the dense engine");
     c->engine = 1;
+    c->sparse_curl = 0;   // the generated sweeps are equal-order
     c->mixed = 1;
   }
   c->NH = c->mixed ? p * (p + 1) * (p + 2) / 6 : c->N;
@@ -1261,7 +1280,10 @@ dgm_status dgm_quadrature_host(int order, int64_t *Q, double *xi, double *w) {
   return DGM_OK;
 }
 
-int dgm_engine(const dgm_ctx *c) { return c ? (c->engine == 1 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE) : -1; }
+int dgm_engine(const dgm_ctx *c) {
+  if (!c) return -1;
+  return c->engine == 0 ? DGM_ENGINE_SPARSE : (c->sparse_curl ? DGM_ENGINE_HYBRID : DGM_ENGINE_DENSE);
+}
 
 int64_t dgm_last_launches(const dgm_ctx *c) { return c ? c->launches : 0; }
 

@@ -108,6 +108,9 @@ struct DenseOps {
   uint64_t *ktlf = nullptr, *ktlb = nullptr;
   int32_t *ktofff = nullptr, *ktoffb = nullptr;
   int ncf = 0;
+  // streamed sparse curl (hybrid engine, dgm_curl.cuh): ĉ scratch [3][n_tet][ldc]
+  double *Cc = nullptr;
+  int ldc = 0;
 };
 
 struct DevProgs {
@@ -162,6 +165,7 @@ struct dgm_ctx {
   int flux = 0;
   int sms = 0;
   int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
+  int sparse_curl = 0; // engine 1 only: the curl by the streamed recurrence sweeps (hybrid engine)
   int mixed = 0;       // 1: H ∈ P^{p-1} (E ∈ P^p), dense engine only; NH = N(p-1)
   int matq = 0;        // 1: ε, μ given at the quadrature points (dense engine, central flux)
   int Q = 0, Qk = 0;   // quadrature points per element (collapsed Gauss–Jacobi, q = p+2), padded
@@ -229,6 +233,13 @@ dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
 // dense-contraction engine (dgm_dense.cu), all orders
 dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
 dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field);
+// streamed lane-per-element curl sweeps (dgm_curl.cuh, generated sweep/curl_p*.cu): ĉ of Y
+constexpr int kCurlPmin = 7, kCurlPmax = 10;
+dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p7(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p8(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p9(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p10(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
 // trace buffers use the 16-element interleaved layout only on the sparse lane path
 inline bool lane_layout(const dgm_ctx *c);
 

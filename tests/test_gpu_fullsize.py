@@ -69,8 +69,10 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-@pytest.mark.parametrize("engine", ["sparse", "dense"])
-@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+FULL = [(n, e) for n in ("C3", "C4", "C5") for e in ("sparse", "dense")] + [("C4", "hybrid"), ("C5", "hybrid")]
+
+
+@pytest.mark.parametrize("name,engine", FULL)
 def test_fullsize_apply_sampled(name, engine):
     cfg, m, c, Ed, Hd, B = _setup(name, engine)
     dE, dH = c.empty_field(), c.empty_field()
@@ -85,8 +87,7 @@ def test_fullsize_apply_sampled(name, engine):
     assert _rel(dH[:, t, :c.N].cpu().numpy(), ref["dH"]) <= TOL
 
 
-@pytest.mark.parametrize("engine", ["sparse", "dense"])
-@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("name,engine", FULL)
 def test_fullsize_one_step_sampled(name, engine):
     from paper_1104_4208_b200.binding import DGM_STEP_CONTINUE
     cfg, m, c, Ed, Hd, B = _setup(name, engine)

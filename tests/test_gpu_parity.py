@@ -44,6 +44,22 @@ def _problem(n, periodic, p, flux, seed=7, materials=True, jitter=0.1):
 ENGINES = ["sparse", "dense"]   # the paper's recurrences / the dense DMMA contractions (include/dgm.h)
 
 
+def engines(p):
+    """Engines that run order p: the hybrid (streamed recurrence curl + DMMA lift and
+    traces) covers orders 7..10."""
+    return ENGINES + (["hybrid"] if 7 <= p <= 10 else [])
+
+
+def combos(ps, extra=None):
+    return [(p, e) for p in ps for e in engines(p)] if extra is None else \
+        [(x, p, e) for x in extra for p in ps for e in engines(p)]
+
+
+def launches_per_step(engine):
+    # stage kernels / (flux, stage GEMM, trace GEMM) / (flux, curl, lift GEMM, trace GEMM), x 2
+    return {"sparse": 2, "dense": 6, "hybrid": 8}[engine]
+
+
 def _ctx(m, rep, p, eps, mu, flux, engine="auto"):
     from paper_1104_4208_b200 import Context
     c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, rep=rep, flux=flux, engine=engine)
@@ -92,24 +108,19 @@ def _apply_parity(case, p, engine):
     return errs
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("p", list(range(1, 11)))
+@pytest.mark.parametrize("p,engine", combos(range(1, 11)))
 def test_apply_parity_all_orders(p, engine):
     errs = _apply_parity("pec-central", p, engine)
     assert max(errs.values()) <= TOL_APPLY, errs
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("case", ["periodic-central", "pec-upwind", "mixed-upwind"])
-@pytest.mark.parametrize("p", [2, 5, 8, 10])
+@pytest.mark.parametrize("case,p,engine", combos([2, 5, 8, 10], ["periodic-central", "pec-upwind", "mixed-upwind"]))
 def test_apply_parity_cases(case, p, engine):
     errs = _apply_parity(case, p, engine)
     assert max(errs.values()) <= TOL_APPLY, errs
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("case,p,engine", combos([2, 3, 4, 5, 6, 7, 8, 9, 10], list(CASES)))
 def test_step_parity_100(case, p, engine):
     """BASELINE north_star: within 1e-10 of the oracle after 100 steps at orders 2-10."""
     periodic, flux, n = CASES[case]
@@ -200,9 +211,7 @@ def test_bad_inputs_fail_loudly():
         Context(m.xyz, m.tet, 2, eps=-1.0)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("case", ["pec-central", "mixed-upwind"])
-@pytest.mark.parametrize("p", [3, 7])
+@pytest.mark.parametrize("case,p,engine", combos([3, 7], ["pec-central", "mixed-upwind"]))
 def test_step_continue_matches_single_call(case, p, engine):
     """DGM_STEP_CONTINUE: k calls of 1 step reusing the trace buffers give the
     same bits as one call of k steps; after dgm_apply_flux the buffers are
@@ -211,7 +220,7 @@ def test_step_continue_matches_single_call(case, p, engine):
     periodic, flux, n = CASES[case]
     m, rep, eps, mu = _problem(n, periodic, p, flux)
     c = _ctx(m, rep, p, eps, mu, flux, engine)
-    per_step = 2 if engine == "sparse" else 6   # stage kernels / (flux, stage GEMM, trace GEMM) x 2
+    per_step = launches_per_step(engine)
     rng = np.random.default_rng(p)
     E = rng.standard_normal((3, m.n_tet, c.N))
     H = rng.standard_normal((3, m.n_tet, c.N))
@@ -228,8 +237,8 @@ def test_step_continue_matches_single_call(case, p, engine):
     assert bool((E1 == E2).all()) and bool((H1 == H2).all())
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("case,p", [("periodic-central", 4), ("pec-upwind", 3), ("mixed-upwind", 8)])
+@pytest.mark.parametrize("case,p,engine", [(c_, p_, e_) for c_, p_ in [("periodic-central", 4), ("pec-upwind", 3),
+                                                                         ("mixed-upwind", 8)] for e_ in engines(p_)])
 def test_step_host_matches_device_step(case, p, engine):
     """dgm_step_host (host buffers, overlapped copies on a side stream) gives the
     same bits as dgm_step on device buffers."""
@@ -283,13 +292,12 @@ def test_spectral_radius_vs_dense_eigen():
     assert not (c.dgm_energy(Ed, Hd) < 1e6 * w0)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine,p", [("sparse", 5), ("dense", 5), ("hybrid", 7), ("hybrid", 10)])
 @pytest.mark.parametrize("flux", ["central", "upwind"])
-def test_single_tet_degenerate_mesh(engine, flux):
+def test_single_tet_degenerate_mesh(engine, p, flux):
     """Degenerate case: one tetrahedron, all four faces PEC (every element tile and
-    16-element group is ragged).  Apply and 20 steps against tier B; a zero-step call
-    is a no-op."""
-    p = 5
+    16-element group is ragged; the hybrid's 32-element sweep group holds one element).
+    Apply and 20 steps against tier B; a zero-step call is a no-op."""
     xyz = np.array([[0.1, 0.0, 0.0], [1.0, 0.1, 0.0], [0.0, 0.9, 0.2], [0.1, 0.2, 1.1]])
     tet = np.array([[0, 1, 2, 3]], dtype=np.int32)
     from paper_1104_4208_b200 import Context
@@ -312,8 +320,8 @@ def test_single_tet_degenerate_mesh(engine, flux):
     assert rel_err(c.to_host(Hd), Hr) <= TOL_STEPS
 
 
-@pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("case,p", [("pec-central", 3), ("mixed-upwind", 4), ("periodic-central", 7)])
+@pytest.mark.parametrize("case,p,engine", [(c_, p_, e_) for c_, p_ in [("pec-central", 3), ("mixed-upwind", 4),
+                                                                         ("periodic-central", 7)] for e_ in engines(p_)])
 def test_graph_replay_matches_single_steps(case, p, engine):
     """Long dgm_step runs replay a captured CUDA graph of 32 steps (launch-bound small
     meshes).  100 steps in one call (3 graph chunks + 4 steps) give the same bits as

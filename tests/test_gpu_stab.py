@@ -43,12 +43,15 @@ def _dev(c, X):
     return D
 
 
-CASES = [(p, (False,) * 3, 2) for p in (1, 2, 3, 4, 5, 6, 7, 8)] + \
-        [(3, (True,) * 3, 3), (6, (False, True, True), 3), (7, (True, False, True), 3)]
+CASES = [(p, (False,) * 3, 2) for p in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10)] + \
+        [(3, (True,) * 3, 3), (6, (False, True, True), 3), (7, (True, False, True), 3), (10, (True,) * 3, 3)]
 
 
-@pytest.mark.parametrize("engine", ["sparse", "dense"])
-@pytest.mark.parametrize("p,periodic,n", CASES)
+def _eng(p):
+    return ["sparse", "dense"] + (["hybrid"] if p >= 7 else [])
+
+
+@pytest.mark.parametrize("p,periodic,n,engine", [c_ + (e_,) for c_ in CASES for e_ in _eng(c_[0])])
 def test_stab_faces_and_rhs_parity(p, periodic, n, engine):
     import torch
     m, c, B, E, H, HF = _case(p, periodic, n, engine=engine)
@@ -67,8 +70,10 @@ def test_stab_faces_and_rhs_parity(p, periodic, n, engine):
     assert w == pytest.approx(B.energy(E, H, HF), rel=1e-12)
 
 
-@pytest.mark.parametrize("engine", ["sparse", "dense"])
-@pytest.mark.parametrize("p,periodic,n", [(2, (False,) * 3, 2), (4, (True,) * 3, 3), (7, (False,) * 3, 2)])
+@pytest.mark.parametrize("p,periodic,n,engine", [c_ + (e_,) for c_ in [(2, (False,) * 3, 2), (4, (True,) * 3, 3),
+                                                                         (7, (False,) * 3, 2), (9, (False,) * 3, 2),
+                                                                         (10, (True,) * 3, 3)]
+                                                   for e_ in _eng(c_[0])])
 def test_stab_steps_parity_and_energy(p, periodic, n, engine):
     """100 symplectic-Euler steps with (H, H^F) advanced together vs the oracle
     (≤1e-10), then the discrete energy stays bounded (leapfrog on a skew system)."""
