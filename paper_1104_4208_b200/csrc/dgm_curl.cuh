@@ -19,12 +19,16 @@
 // holds NPAIR pairs working on the same m (4 groups of 32 elements), so its 8 warps
 // run two instruction streams in near lockstep.
 //
-// Measured at p = 10, C5 (tools/curlbench, ms per launch): coefficients through the
-// constant bank with the warps spread over all directions 19.4 (the ~5k distinct
-// values thrash the constant cache); the same with the CTA's pairs on one m 7.5; a
-// shared-memory coefficient table 8.8; immediates 5.8 (this version).  Splitting ĉ by
-// sign so that every warp of a CTA runs the same direction without barriers (two
-// output buffers, twice the output writes) 8.4.
+// Measured at p = 10, C5 (tools/curlbench, ms per launch; earlier session): coefficients
+// through the constant bank with the warps spread over all directions 19.4; the same
+// with the CTA's pairs on one m 7.5; a shared-memory coefficient table 8.8; immediates
+// 5.8.  Splitting ĉ by sign so that every warp of a CTA runs the same direction without
+// barriers (two output buffers, twice the output writes) 8.4.  Round 2, same binary
+// harness on one box (profiles/r02_curl_variants.txt): immediates 8.06, the constant
+// table in order of first use (gen/sweepgen.py Consts, the default) 6.73; a CTA-wide
+// lockstep barrier instead of the pair barrier changes neither.  The sweeps sit at
+// 8-10% of the FP64 pipe: 255 registers (a two-degree-level window of u per lane) leave
+// two warps per scheduler, and every instruction-line fetch or constant load is exposed.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -57,7 +61,11 @@ __device__ __forceinline__ void wait_groups() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NW) : "memory");
 }
 // named barrier of warp pair q (ids 1..NPAIR; 0 is __syncthreads)
+#ifdef CURL_CTA_SYNC   // experiments: all pairs of the CTA in lockstep (one named barrier of the CTA)
+__device__ __forceinline__ void pair_barrier(int) { asm volatile("bar.sync 1, %0;\n" ::"n"(64 * NPAIR) : "memory"); }
+#else
 __device__ __forceinline__ void pair_barrier(int q) { asm volatile("bar.sync %0, 64;\n" ::"r"(q + 1) : "memory"); }
+#endif
 
 template <int P>
 struct Dims {

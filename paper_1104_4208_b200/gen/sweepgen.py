@@ -54,19 +54,35 @@ def ldc_of(p):
 
 
 class Consts:
-    """Coefficients as 64-bit immediates (ptxas materialises them with two uniform
-    moves; measured faster than the constant bank, whose cache the ~5k distinct values
-    of p = 10 thrash, and than a shared-memory table)."""
-    def __init__(self, p):
+    """Coefficients of the sweeps.  Default "const": one __constant__ table per order
+    (distinct |values| in order of first use, 39 KB at p = 10), which ptxas reads with
+    uniform constant loads (LDCU.128, two coefficients per load).  "imm": 64-bit
+    immediates (two uniform moves per coefficient).  Measured at p = 10 on the C5 mesh
+    (tools/curlbench, profiles/r02_curl_variants.txt): const 6.73 ms, imm 8.06 ms per
+    launch; imm spends 10 of 16 cycles per issue in no-instruction stalls (a 128-byte
+    instruction line every 8 instructions, 29k instructions), const 4.5 of 15 (18.6k
+    instructions) with constant-load waits (short scoreboard 8.6) the new top stall."""
+    def __init__(self, p, mode=None):
         self.p, self.vals = p, set()
+        self.mode = mode or os.environ.get("SWEEP_COEF", "const")
+        self.table, self.index = [], {}
 
     def ref(self, x):
         a = abs(float(x))
         self.vals.add(a)
+        if self.mode == "const":
+            if a not in self.index:
+                self.index[a] = len(self.table)
+                self.table.append(a)
+            return f"kC{self.p}[{self.index[a]}]", float(x) < 0
         bits = struct.unpack("<Q", struct.pack("<d", a))[0]
         return f"dgm::curl::kimm<0x{bits:016x}ull>()", float(x) < 0
 
     def emit(self):
+        if self.mode == "const":
+            body = ",\n".join(", ".join(repr(v) for v in self.table[i:i + 4]) for i in range(0, len(self.table), 4))
+            return (f"// {len(self.vals)} distinct |coefficients|, constant bank in order of first use\n"
+                    f"__constant__ double kC{self.p}[{len(self.table)}] = {{\n{body}}};")
         return f"// {len(self.vals)} distinct |coefficients|, as immediates"
 
 

@@ -259,22 +259,47 @@ def test_step_host_matches_device_step(case, p, engine):
     assert torch.equal(Eh, Ed.cpu()) and torch.equal(Hh, Hd.cpu())
 
 
+def _dense_K(m, rep, p, eps, mu, flux):
+    """K = -Mμ^{-1} C_HE Mε^{-1} C_EH from the tier-A coupling blocks (the power
+    iteration applies Ė(0,H) then Ḣ(·,0), so the upwind self-terms, which act on the
+    field being updated, are zero there) and its dominant eigenvalue modulus."""
+    A = TierA(m.xyz, m.tet, rep, p, eps, mu, flux=flux)
+    o = A.ops
+    import scipy.linalg as sl
+    Meps = sl.block_diag(*o["Meps"])
+    Mmu = sl.block_diag(*o["Mmu"])
+    C = (o["HE_vol"] + o["HE_face"]).toarray()
+    EH = (o["EH_vol"] + o["EH_face"]).toarray()     # = -Cᵀ for the central flux
+    K = -np.linalg.solve(Mmu, C @ np.linalg.solve(Meps, EH))
+    ev = np.linalg.eigvals(K)
+    return np.max(np.abs(ev)), ev
+
+
+@pytest.mark.parametrize("p,flux,periodic", [(4, "central", (False,) * 3), (4, "upwind", (False,) * 3),
+                                             (3, "upwind", (True, False, False))])
+def test_spectral_radius_orders_and_upwind(p, flux, periodic):
+    """NEXT-3 at p >= 3 and with the upwind flux: the GPU power
+    iteration against the dense eigensolve of the tier-A coupling operator.  For the
+    upwind flux with ε, μ varying per element, the coupling weights Z⁺/(Z⁻+Z⁺) make K
+    non-symmetric; its dominant eigenvalue is still real and simple here (asserted),
+    so the Rayleigh quotient converges to it."""
+    m, rep, eps, mu = _problem((3, 2, 2) if any(periodic) else 2, periodic, p, flux)
+    lam, ev = _dense_K(m, rep, p, eps, mu, flux)
+    top = ev[np.argmax(np.abs(ev))]
+    assert abs(top.imag) < 1e-8 * lam and top.real > 0
+    c = _ctx(m, rep, p, eps, mu, flux)
+    rho = c.dgm_spectral_radius(1500, seed=5)
+    assert rho == pytest.approx(lam, rel=5e-3)
+
+
 def test_spectral_radius_vs_dense_eigen():
     """NEXT-3: the GPU power iteration finds the largest
     eigenvalue of K = Mμ^{-1} C Mε^{-1} Cᵀ, checked against a dense eigensolve of
     the tier-A matrices, and Δt = 2/√ρ is the stability boundary (reading G6)."""
     p = 2
     m, rep, eps, mu = _problem(2, (False,) * 3, p, "central")
-    A = TierA(m.xyz, m.tet, rep, p, eps, mu)
-    o = A.ops
-    n, nd = m.n_tet, 3 * A.N
-    import scipy.linalg as sl
-    Meps = sl.block_diag(*o["Meps"])
-    Mmu = sl.block_diag(*o["Mmu"])
-    C = (o["HE_vol"] + o["HE_face"]).toarray()
-    EH = (o["EH_vol"] + o["EH_face"]).toarray()     # = -Cᵀ
-    K = -np.linalg.solve(Mmu, C @ np.linalg.solve(Meps, EH))
-    lam = np.max(np.abs(np.linalg.eigvals(K)))
+    lam, _ = _dense_K(m, rep, p, eps, mu, "central")
+    n = m.n_tet
     c = _ctx(m, rep, p, eps, mu, "central")
     rho = c.dgm_spectral_radius(400, seed=3)
     assert rho == pytest.approx(lam, rel=2e-3)
