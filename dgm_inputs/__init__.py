@@ -199,3 +199,29 @@ def config_materials(name: str, n_tet: int):
     else:
         eps = np.full(n_tet, c["eps"][1])
     return eps, np.ones(n_tet)
+
+
+def curved_mesh(m: Mesh, delta: float, amp=(1.0, -0.8, 0.6)):
+    """Curved (quadratic, 10-node) version of a mesh: every point x of the straight mesh
+    moves by d(x) = delta * amp * Π_a sin(2π (x_a - lo_a) / (hi_a - lo_a)), which is zero
+    on every boundary plane of the box (the domain and its flat boundary are unchanged)
+    and periodic (images move together).  Vertices are the moved vertices; the edge
+    nodes are the moved midpoints of the straight edges, computed per global edge, so
+    neighbours share them bit for bit.  Returns (mesh with moved vertices,
+    edge_nodes [n_tet, 6, 3]) with the edges (0,1) (0,2) (0,3) (1,2) (1,3) (2,3) of the
+    local vertex order.  Pure geometry: no arithmetic of the method."""
+    lo = np.array([b[0] for b in m.box])
+    hi = np.array([b[1] for b in m.box])
+    a = np.asarray(amp, dtype=np.float64)
+
+    def move(x):
+        s = np.prod(np.sin(2.0 * np.pi * (x - lo) / (hi - lo)), axis=-1)
+        return x + delta * s[..., None] * a
+
+    X = m.xyz[m.tet]                                            # [n, 4, 3] straight
+    pairs = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+    mids = np.stack([0.5 * (X[:, i] + X[:, j]) for i, j in pairs], axis=1)
+    edge_nodes = move(mids)
+    out = Mesh(xyz=np.ascontiguousarray(move(m.xyz)), tet=m.tet, rep=m.rep, periodic=m.periodic, shape=m.shape,
+               box=m.box, info=dict(m.info, curved_delta=delta, curved_amp=tuple(amp)))
+    return out, np.ascontiguousarray(edge_nodes)

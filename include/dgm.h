@@ -90,8 +90,8 @@ typedef struct {
  *           lane-per-element sweeps on the FP64 pipes, written to an
  *           internal ĉ buffer and added in the epilogue of the DENSE stage GEMM, which
  *           then applies only the lift; traces as in DENSE.  4 launches per stage.
- *   AUTO:   SPARSE for p <= 5, DENSE for p >= 6 (measured fastest there; HYBRID ties
- *           DENSE at p = 8 and is 2% slower at p = 10).  Mixed orders use DENSE.
+ *   AUTO:   SPARSE for p <= 5, DENSE for p = 6, HYBRID for p >= 7 (measured fastest
+ *           there).  Mixed orders use DENSE.
  * The environment variable DGM_ENGINE=sparse|dense|hybrid overrides AUTO.  For measurements,
  * DGM_STAGE_NH / DGM_TRACE_NH = 1|2 force the dense GEMM tile width (one or two 96-column
  * warp columns; default one) and DGM_TILE_ORDER=0 the static GEMM tile order
@@ -119,6 +119,26 @@ typedef struct {
                             points -> × ŵ_i / m(x_i) -> back to the modes.  Central
                             flux, equal orders, dense engine (AUTO resolves to it);
                             dgm_energy and dgm_spectral_radius are not available. */
+  const double *edge_nodes; /* NULL: flat (affine) elements.  Else curved elements
+                            ("Curved elements"): host
+                            [n_tet][6][3] physical coordinates of the edge nodes of a
+                            quadratic (10-node) tetrahedron, edges (0,1) (0,2) (0,3)
+                            (1,2) (1,3) (2,3) of the tet's local vertex order.  The
+                            map Φ(x̂) = Σ_a λ_a(2λ_a-1) X_a + Σ_ab 4 λ_a λ_b X_ab
+                            (λ: barycentric coordinates of x̂ on v̂0..v̂3) is
+                            non-affine; the curl and face terms stay geometry-free
+                            (covariant identities, hold pointwise
+                            for any smooth Φ) and the full mass with |det F(x̂)| m
+                            F⁻¹F⁻ᵀ(x̂) is replaced by the reverse-numerical-integration
+                            approximate inverse: residual -> point values -> × ŵ_i
+                            F(x̂_i)ᵀF(x̂_i) / (m(x_i) det F(x̂_i)) (a 3x3 mix per
+                            point) -> back to the modes.  Central flux, equal orders,
+                            dense engine; m = eps/mu per element or scalar, or at the
+                            points (material_points; x_i = Φ(ξ_i)).  sign det F(x̂_i)
+                            must be the same at every quadrature point (else
+                            DGM_EMESH); dgm_energy and dgm_spectral_radius are not
+                            available.  Neighbours must share their face's edge
+                            nodes (checked on non-periodic interior faces). */
 } dgm_opts;
 
 /* Validate the mesh, match faces, compute per-element geometry

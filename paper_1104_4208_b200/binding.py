@@ -38,7 +38,7 @@ class _Mesh(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("flux", ctypes.c_int32), ("eps_per_elem", ctypes.c_int32), ("mu_per_elem", ctypes.c_int32),
                 ("alpha0", ctypes.c_double), ("engine", ctypes.c_int32), ("mixed_order", ctypes.c_int32),
-                ("material_points", ctypes.c_int32)]
+                ("material_points", ctypes.c_int32), ("edge_nodes", ctypes.c_void_p)]
 
 
 _lib = None
@@ -137,7 +137,7 @@ class Context:
     """Owns a dgm_ctx.  Methods mirror the C ABI names (dgm_*)."""
 
     def __init__(self, xyz, tet, p, eps=1.0, mu=1.0, rep=None, flux="central", alpha0=1.0, engine="auto",
-                 mixed_order=False, material_points=False):
+                 mixed_order=False, material_points=False, edge_nodes=None):
         lib = load_library()
         self._lib = lib
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
@@ -155,8 +155,14 @@ class Context:
             if eps_a.size != nq or mu_a.size != nq:
                 raise ValueError(f"material_points: eps and mu must hold n_tet*Q = {nq} values")
             self._keep = (xyz, tet, repa, eps_a, mu_a)
+        en = None
+        if edge_nodes is not None:   # curved (quadratic) elements: [n_tet, 6, 3] edge-node coordinates
+            en = np.ascontiguousarray(edge_nodes, dtype=np.float64)
+            if en.shape != (tet.shape[0], 6, 3):
+                raise ValueError(f"edge_nodes must have shape (n_tet, 6, 3), got {en.shape}")
+            self._keep = self._keep + (en,)
         o = _Opts(FLUX[flux], int(eps_a.size > 1), int(mu_a.size > 1), float(alpha0), ENGINE[engine],
-                  int(bool(mixed_order)), int(bool(material_points)))
+                  int(bool(mixed_order)), int(bool(material_points)), None if en is None else en.ctypes.data)
         # H's live modes: N(p-1) for mixed orders (E ∈ P^p, H ∈ P^{p-1}), else N
         self.NH = p * (p + 1) * (p + 2) // 6 if mixed_order else (p + 1) * (p + 2) * (p + 3) // 6
         h = ctypes.c_void_p()

@@ -92,6 +92,7 @@ struct GemmArgs {
   double *raw;
   int rawld, rawNk;
   int unit_m;
+  int no_geo;   // EPI_STAGE: no G' mix (curved elements: the per-point factors carried it)
   unsigned long long *tile_ctr;   // dynamic tile counter [claims, arrivals] (self-resetting), or null: static order
   // EPI_STAGE, hybrid engine: the curl ĉ from the streamed sweeps is added to the
   // accumulator, ĉ[c][e][b] at cc + c*ccs + e*ldc + b for b < ncc (else 0)
@@ -384,9 +385,9 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
             rw[2 * g.rawNk] = v2;
             continue;
           }
-          const double x0 = cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
-          const double x1 = cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
-          const double x2 = cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
+          const double x0 = g.no_geo ? cm * v0 : cm * (G[0] * v0 + G[1] * v1 + G[2] * v2);
+          const double x1 = g.no_geo ? cm * v1 : cm * (G[1] * v0 + G[3] * v1 + G[4] * v2);
+          const double x2 = g.no_geo ? cm * v2 : cm * (G[2] * v0 + G[4] * v1 + G[5] * v2);
           const double sc = upd ? g.dt : 1.0;
           out[o[u]] = xv[u][0] + sc * x0;
           out[cs + o[u]] = xv[u][1] + sc * x1;
@@ -614,9 +615,12 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     f.n_tet = c->n_tet;
     f.ncols = 3 * Qk;
     f.tr = D.P;
-    f.scale = a.stage == STAGE_E ? D.SWe : D.SWm;
+    f.scale = c->curved ? nullptr : (a.stage == STAGE_E ? D.SWe : D.SWm);
     f.sQ = Qk;
     if ((s = gemm_go<EPI_TRACE>(c, f, st)) != DGM_OK) return s;
+    // curved elements: the per-point 3x3 factor ŵ_i F(ξ_i)ᵀF(ξ_i)/(m det F(ξ_i)) replaces
+    // ŵ_i/m(x_i) here and the element's G' after the back transform
+    if (c->curved && (s = launch_pointmix(c, D.P, a.stage == STAGE_E ? D.KE : D.KH, st)) != DGM_OK) return s;
     GemmArgs b = g;
     b.raw = nullptr;
     b.cc = nullptr;   // ĉ entered the residual already
@@ -632,6 +636,7 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     b.ktl = D.ktlb;
     b.ktoff = D.ktoffb;
     b.unit_m = 1;
+    b.no_geo = c->curved;
     if ((s = gemm_go<EPI_STAGE>(c, b, st)) != DGM_OK) return s;
   } else {
     dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
@@ -639,6 +644,35 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
   }
   if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st, v);
   return DGM_OK;
+}
+
+namespace {
+// curved elements: the 3x3 point factor of the approximate inverse
+// mass on the point values of the residual, one thread per (element, point)
+__global__ void pointmix_kernel(double *__restrict__ P, const double *__restrict__ K, int64_t n_tet, int Q, int Qk) {
+  const int64_t total = n_tet * Q;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / Q;
+    const int q = (int)(i - e * Q);
+    double *pe = P + e * 3 * (int64_t)Qk + q;
+    const double *k = K + (e * Qk + q) * 6;
+    const double v0 = pe[0], v1 = pe[Qk], v2 = pe[2 * Qk];
+    pe[0] = k[0] * v0 + k[1] * v1 + k[2] * v2;
+    pe[Qk] = k[1] * v0 + k[3] * v1 + k[4] * v2;
+    pe[2 * Qk] = k[2] * v0 + k[4] * v1 + k[5] * v2;
+  }
+}
+}  // namespace
+
+dgm_status launch_pointmix(dgm_ctx *c, double *P, const double *K, cudaStream_t st) {
+  const int64_t total = c->n_tet * c->Q;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 16 * (int64_t)c->sms) grid = 16 * (int64_t)c->sms;
+  if (grid < 1) return DGM_OK;
+  pointmix_kernel<<<(unsigned)grid, 256, 0, st>>>(P, K, c->n_tet, c->Q, c->Qk);
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("pointmix_kernel: ") + cudaGetErrorString(e));
 }
 
 dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st) {

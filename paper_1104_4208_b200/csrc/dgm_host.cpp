@@ -555,7 +555,9 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
                up((void **)&D.ktlf, lf.data(), lf.size() * 8) && up((void **)&D.ktofff, of.data(), of.size() * 4) &&
                up((void **)&D.ktlb, lb.data(), lb.size() * 8) && up((void **)&D.ktoffb, ob.data(), ob.size() * 4) &&
                up((void **)&D.SWe, c->h_swe.data(), c->h_swe.size() * 8) &&
-               up((void **)&D.SWm, c->h_swm.data(), c->h_swm.size() * 8);
+               up((void **)&D.SWm, c->h_swm.data(), c->h_swm.size() * 8) &&
+               (!c->curved || (up((void **)&D.KE, c->h_ke.data(), c->h_ke.size() * 8) &&
+                               up((void **)&D.KH, c->h_kh.data(), c->h_kh.size() * 8)));
     if (!okm) return dgm::set_err(c, DGM_ENOMEM, "dense_build: material-point operators");
     D.ncf = ncf;
     CUDA_TRY(c, cudaMalloc(&D.AC, sizeof(double) * 3 * (size_t)Nk * (size_t)(n_or1(c))));
@@ -587,7 +589,7 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->dense.Cc);
   for (void *q : {(void *)c->dense.Bf, (void *)c->dense.Bb, (void *)c->dense.ktlf, (void *)c->dense.ktofff,
                   (void *)c->dense.ktlb, (void *)c->dense.ktoffb, (void *)c->dense.SWe, (void *)c->dense.SWm,
-                  (void *)c->dense.AC, (void *)c->dense.P})
+                  (void *)c->dense.AC, (void *)c->dense.P, (void *)c->dense.KE, (void *)c->dense.KH})
     cudaFree(q);
   cudaFree(c->d_stream);
   cudaFree(c->d_geo);
@@ -618,7 +620,7 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   if (order < 1 || order > DGM_PMAX)
     return dgm::set_err(c, DGM_EORDER, "order " + std::to_string(order) + " outside 1.." + std::to_string(DGM_PMAX));
   if (m->n_tet > (int64_t)INT32_MAX / 4) return dgm::set_err(c, DGM_EINVAL, "too many tets");
-  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0, 0};
+  dgm_opts o = opts ? *opts : dgm_opts{DGM_FLUX_CENTRAL, 0, 0, 0.0, DGM_ENGINE_AUTO, 0, 0, nullptr};
   if (o.engine < DGM_ENGINE_AUTO || o.engine > DGM_ENGINE_HYBRID) return dgm::set_err(c, DGM_EINVAL, "unknown engine");
   if (o.flux != DGM_FLUX_CENTRAL && o.flux != DGM_FLUX_UPWIND && o.flux != DGM_FLUX_STABILIZED)
     return dgm::set_err(c, DGM_EINVAL, "unknown flux");
@@ -631,11 +633,12 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   c->n_tet = n;
   c->flux = o.flux;
   // engine: explicit option, else DGM_ENGINE, else by order (measured): the
-  // sparse recurrence kernels for p <= 5, dense DMMA contractions for p >= 6 (the hybrid,
-  // streamed recurrence curl + DMMA lift and traces, ties at p = 8 and loses 2% at p = 10)
+  // sparse recurrence kernels for p <= 5, dense DMMA contractions at p = 6, and from p = 7
+  // the hybrid (the curl by the streamed recurrence sweeps, DMMA lift and traces; with the
+  // constant-table sweeps C4 5.79 vs 5.84 ms and C5 46.9 vs 48.3 ms per step against dense)
   int kind = o.engine;
   if (kind == DGM_ENGINE_AUTO) {
-    kind = p >= 6 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE;
+    kind = p >= dgm::kCurlPmin ? DGM_ENGINE_HYBRID : p >= 6 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE;
     if (const char *v = std::getenv("DGM_ENGINE"))
       kind = std::strcmp(v, "dense") == 0 ? DGM_ENGINE_DENSE
              : std::strcmp(v, "hybrid") == 0 && p >= dgm::kCurlPmin ? DGM_ENGINE_HYBRID
@@ -678,6 +681,21 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
         c->h_swe[(size_t)t * c->Qk + i] = w[i] / e;   // quadrature weight / material
         c->h_swm[(size_t)t * c->Qk + i] = w[i] / u;
       }
+  }
+  // curved (quadratic) elements: the same point pipeline with a 3x3 mix per point
+  if (o.edge_nodes) {
+    if (o.flux != DGM_FLUX_CENTRAL) return dgm::set_err(c, DGM_EINVAL, "curved elements: central flux only");
+    if (o.mixed_order) return dgm::set_err(c, DGM_EINVAL, "curved elements: not with mixed orders");
+    if (o.engine == DGM_ENGINE_SPARSE) return dgm::set_err(c, DGM_EINVAL, "curved elements need the dense engine");
+    c->engine = 1;
+    c->matq = 1;
+    c->curved = 1;
+    if (!o.material_points) {
+      std::vector<double> xi, w;
+      tet_quadrature(p, xi, w);
+      c->Q = (int)w.size();
+      c->Qk = (c->Q + 15) / 16 * 16;
+    }
   }
   auto rep = [&](int32_t v) -> int64_t { return m->rep ? (int64_t)m->rep[v] : (int64_t)v; };
 
@@ -761,6 +779,73 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
       }
     }
   }
+  // ---- curved elements: per quadrature point ξ_i the Jacobian F(ξ_i) of the quadratic
+  // map and the point factor of the approximate inverse mass:
+  //   K_i = ŵ_i F(ξ_i)ᵀF(ξ_i) / (m(x_i) det F(ξ_i))   (6 entries, symmetric)
+  // the affine case gives K_i = ŵ_i G'/m, i.e. the flat path's G' and ŵ_i/m
+  if (c->curved) {
+    std::vector<double> xi, w;
+    tet_quadrature(p, xi, w);
+    const int Q = c->Q, Qk = c->Qk;
+    c->h_ke.assign((size_t)n * Qk * 6, 0.0);
+    c->h_kh.assign((size_t)n * Qk * 6, 0.0);
+    static const int E[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    static const double GL[4][3] = {{-1, -1, -1}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1}};   // ∇λ_a
+    for (int64_t t = 0; t < n; ++t) {
+      double X[10][3];   // vertices, then edge nodes
+      double L = 0;
+      for (int k = 0; k < 4; ++k)
+        for (int i = 0; i < 3; ++i) X[k][i] = m->xyz[3 * (int64_t)m->tet[4 * t + k] + i];
+      for (int e = 0; e < 6; ++e)
+        for (int i = 0; i < 3; ++i) {
+          X[4 + e][i] = o.edge_nodes[(t * 6 + e) * 3 + i];
+          if (!std::isfinite(X[4 + e][i]))
+            return dgm::set_err(c, DGM_EINVAL, "tet " + std::to_string(t) + ": non-finite edge node");
+        }
+      for (int a = 0; a < 4; ++a)
+        for (int b = a + 1; b < 4; ++b) {
+          double d2 = 0;
+          for (int i = 0; i < 3; ++i) d2 += (X[a][i] - X[b][i]) * (X[a][i] - X[b][i]);
+          L = std::max(L, std::sqrt(d2));
+        }
+      for (int q = 0; q < Q; ++q) {
+        const double *x = &xi[3 * q];
+        const double lam[4] = {1.0 - x[0] - x[1] - x[2], x[0], x[1], x[2]};
+        double F[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};   // F[i][j] = ∂Φ_i/∂ξ_j
+        for (int j = 0; j < 3; ++j) {
+          for (int a = 0; a < 4; ++a) {
+            const double d = (4.0 * lam[a] - 1.0) * GL[a][j];
+            for (int i = 0; i < 3; ++i) F[i][j] += d * X[a][i];
+          }
+          for (int e = 0; e < 6; ++e) {
+            const int a = E[e][0], b = E[e][1];
+            const double d = 4.0 * (GL[a][j] * lam[b] + lam[a] * GL[b][j]);
+            for (int i = 0; i < 3; ++i) F[i][j] += d * X[4 + e][i];
+          }
+        }
+        const double det = F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) -
+                           F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+                           F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+        if (!(std::fabs(det) > 1e-12 * L * L * L) || (det > 0) != (sgn[t] > 0))
+          return dgm::set_err(c, DGM_EMESH, "tet " + std::to_string(t) + ": curved map folds (det F changes sign)");
+        double G[6];
+        const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+        for (int k = 0; k < 6; ++k) {
+          double sum = 0;
+          for (int i = 0; i < 3; ++i) sum += F[i][ij[k][0]] * F[i][ij[k][1]];
+          G[k] = sum / det;
+        }
+        const double me = o.material_points ? eps[t * Q + q] : o.eps_per_elem ? eps[t] : eps[0];
+        const double mu_ = o.material_points ? mu[t * Q + q] : o.mu_per_elem ? mu[t] : mu[0];
+        if (!(me > 0) || !(mu_ > 0) || !std::isfinite(me) || !std::isfinite(mu_))
+          return dgm::set_err(c, DGM_EINVAL, "tet " + std::to_string(t) + ": eps/mu must be positive");
+        for (int k = 0; k < 6; ++k) {
+          c->h_ke[((size_t)t * Qk + q) * 6 + k] = w[q] * G[k] / me;
+          c->h_kh[((size_t)t * Qk + q) * 6 + k] = w[q] * G[k] / mu_;
+        }
+      }
+    }
+  }
   // ---- face matching: sort representative triples (deterministic)
   std::vector<FaceRec> faces;
   try {
@@ -806,6 +891,30 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   }
   for (int64_t t = 0; t < n; ++t)
     for (int f = 0; f < 4; ++f) c->sign[4 * t + f] = (int8_t)((f % 2 == 0 ? 1 : -1) * sgn[t]);
+  // curved elements: a face shared by two tets through the same three vertices must have
+  // the same three edge nodes on both sides (conforming curved faces; periodic pairs
+  // are the caller's responsibility)
+  if (c->curved) {
+    auto edge_of = [](int a, int b) { return a == 0 ? b - 1 : (a == 1 ? 2 + b - 1 : 5); };   // a < b
+    for (int64_t t = 0; t < n; ++t)
+      for (int f = 0; f < 4; ++f) {
+        const int32_t s2 = c->nbr[4 * t + f];
+        if (s2 < 0 || s2 < t) continue;
+        const int g = c->nbrf[4 * t + f];
+        const int *fa = kFaceVerts[f], *fb = kFaceVerts[g];
+        bool same = true;
+        for (int k = 0; k < 3; ++k) same &= m->tet[4 * t + fa[k]] == m->tet[4 * (int64_t)s2 + fb[k]];
+        if (!same) continue;   // periodic pair
+        for (int u = 0; u < 3; ++u)
+          for (int v = u + 1; v < 3; ++v) {
+            const double *pa = &o.edge_nodes[(t * 6 + edge_of(fa[u], fa[v])) * 3];
+            const double *pb = &o.edge_nodes[((int64_t)s2 * 6 + edge_of(fb[u], fb[v])) * 3];
+            if (pa[0] != pb[0] || pa[1] != pb[1] || pa[2] != pb[2])
+              return dgm::set_err(c, DGM_EMESH, "tets " + std::to_string(t) + ", " + std::to_string(s2) +
+                                                    ": shared face with different edge nodes");
+          }
+      }
+  }
 
   // ---- stabilised central flux: face numbering and face geometry
   if (o.flux == DGM_FLUX_STABILIZED) {

@@ -105,6 +105,8 @@ struct DenseOps {
   // values, Bb [3Qk][nc1] point values -> modes; SWe/SWm [n][Qk] = ŵ_i / ε, μ at the
   // points; AC [n][3Nk] residual scratch, P [n][3Qk] point-value scratch
   double *Bf = nullptr, *Bb = nullptr, *SWe = nullptr, *SWm = nullptr, *AC = nullptr, *P = nullptr;
+  // curved elements: per point K_i = ŵ_i F(ξ_i)ᵀF(ξ_i) / (m det F(ξ_i)), [n][Qk][6] (E: ε, H: μ)
+  double *KE = nullptr, *KH = nullptr;
   uint64_t *ktlf = nullptr, *ktlb = nullptr;
   int32_t *ktofff = nullptr, *ktoffb = nullptr;
   int ncf = 0;
@@ -167,9 +169,10 @@ struct dgm_ctx {
   int engine = 0;      // 0: sparse recurrence kernels, 1: dense DMMA contractions (DGM_ENGINE=dense)
   int sparse_curl = 0; // engine 1 only: the curl by the streamed recurrence sweeps (hybrid engine)
   int mixed = 0;       // 1: H ∈ P^{p-1} (E ∈ P^p), dense engine only; NH = N(p-1)
-  int matq = 0;        // 1: ε, μ given at the quadrature points (dense engine, central flux)
+  int matq = 0;        // 1: the point pipeline of the inverse mass (material points or curved elements)
+  int curved = 0;      // 1: curved (quadratic) elements, per-point 3x3 factors h_ke / h_kh
   int Q = 0, Qk = 0;   // quadrature points per element (collapsed Gauss–Jacobi, q = p+2), padded
-  std::vector<double> h_swe, h_swm;
+  std::vector<double> h_swe, h_swm, h_ke, h_kh;
   int NH = 0;
   dgm::DenseOps dense{};
   void *d_dense = nullptr;
@@ -233,6 +236,8 @@ dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
 // dense-contraction engine (dgm_dense.cu), all orders
 dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
 dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field);
+// curved elements: P[e][c Qk + i] <- Σ_l K[e][i][c,l] P[e][l Qk + i]
+dgm_status launch_pointmix(dgm_ctx *c, double *P, const double *K, cudaStream_t st);
 // streamed lane-per-element curl sweeps (dgm_curl.cuh, generated sweep/curl_p*.cu): ĉ of Y
 constexpr int kCurlPmin = 7, kCurlPmax = 10;
 dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
