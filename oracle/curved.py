@@ -161,3 +161,49 @@ def curved_oracle(xyz, tet, rep, p, edge_nodes, eps=1.0, mu=1.0):
     B = TierBCurved(xyz, tet, rep, p, edge_nodes, eps, mu)
     B._m_src = {"E": eps, "H": mu}
     return B
+
+
+def project_curved(B: TierBCurved, f, q=None):
+    """L²(ε = 1) projection of a field f: x[...,3] -> [...,3] onto the covariant space
+    of curved elements: per element M_full Ê = b with b_{β,m} = ∫_T̂ |det F|
+    (F^{-1} f(Φ(x̂)))_m φ_β dx̂ (test functions e = F^{-T} φ_β e_m), both by the
+    high-order rule.  Returns [3, n_tet, N]."""
+    qq = q or (B.p + 8)
+    pts, w = tet_rule(qq)
+    V = phi(B.p, pts)
+    out = np.empty((3, B.n_tet, B.N))
+    for T in range(B.n_tet):
+        Fq = p2_jacobian(B.nodes[T:T + 1], pts)[0]
+        det = np.abs(np.linalg.det(Fq))
+        Finv = np.linalg.inv(Fq)
+        x = p2_map(B.nodes[T:T + 1], pts)[0]
+        g = np.einsum("qij,qj->qi", Finv, f(x))                                 # F^{-1} f
+        b = np.concatenate([V @ (w * det * g[:, l]) for l in range(3)])
+        Gm = np.einsum("qik,qjk->qij", Finv, Finv)
+        M = _mass_unit(V, w * det, Gm, B.N)
+        out[:, T] = np.linalg.solve(M, b).reshape(3, B.N)
+    return out
+
+
+def _mass_unit(V, w, Gm, N):
+    M = np.empty((3 * N, 3 * N))
+    for l in range(3):
+        for k in range(3):
+            M[l * N:(l + 1) * N, k * N:(k + 1) * N] = (V * (w * Gm[:, l, k])[None, :]) @ V.T
+    return M
+
+
+def energy_curved(B: TierBCurved, X, q=None):
+    """½ Σ_T X_Tᵀ M_full X_T with ε = 1 (the exact curved L² norm of the field)."""
+    qq = q or (B.p + 8)
+    pts, w = tet_rule(qq)
+    V = phi(B.p, pts)
+    tot = 0.0
+    for T in range(B.n_tet):
+        Fq = p2_jacobian(B.nodes[T:T + 1], pts)[0]
+        det = np.abs(np.linalg.det(Fq))
+        Finv = np.linalg.inv(Fq)
+        Gm = np.einsum("qik,qjk->qij", Finv, Finv)
+        x = X[:, T].reshape(-1)
+        tot += x @ _mass_unit(V, w * det, Gm, B.N) @ x
+    return 0.5 * tot

@@ -108,7 +108,7 @@ def test_curved_rejects_bad_input():
     with pytest.raises(DgmError):
         Context(cm.xyz, cm.tet, 2, edge_nodes=en, engine="sparse")
     bad = en.copy()   # a neighbour's copy of a shared edge node differs
-    bad[0, 3] += 1e-3
+    bad[0] += 1e-3
     with pytest.raises(DgmError, match="edge nodes"):
         Context(cm.xyz, cm.tet, 2, edge_nodes=bad)
     fold = en.copy()   # an edge node pulled far across the element: det F changes sign

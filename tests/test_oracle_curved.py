@@ -125,3 +125,31 @@ def test_curved_mesh_keeps_the_box():
     for r in np.unique(m.rep):
         idx = np.nonzero(m.rep == r)[0]
         assert np.abs(d[idx] - d[idx[0]]).max() < 1e-15
+
+
+def _curved_cavity_error(p, delta, t_end=0.2, nsteps=200):
+    from oracle import fields
+    from oracle.curved import project_curved, energy_curved
+    from oracle.timestep import symplectic_euler
+    m = di.kuhn_mesh(2, jitter=0.0)
+    cm, en = di.curved_mesh(m, delta)
+    B = curved_oracle(cm.xyz, cm.tet, None, p, en, 1.0, 1.0)
+    dt = t_end / nsteps
+    E0, _ = fields.cavity110(0.0)
+    _, Hh = fields.cavity110(-0.5 * dt)
+    E, H = project_curved(B, E0), project_curved(B, Hh)
+    E, H, _ = symplectic_euler(B, E, H, dt, nsteps)
+    Ee, _ = fields.cavity110(t_end)
+    ref = project_curved(B, Ee)
+    return np.sqrt(energy_curved(B, ref - E) / energy_curved(B, ref))
+
+
+def test_curved_cavity_mode_converges_in_p():
+    """Physics pin: the PEC unit cube meshed with curved elements (interior warp, the
+    boundary stays flat) carries the analytic TE mode (1,1,0) (PAPER.md:242-269 cavity;
+    oracle.fields.cavity110).  Projected with the exact curved mass and stepped with
+    the curved operator, the relative L² error after t = 0.2 falls by >= 3x per order
+    (p = 2, 3, 4): 7.1e-2, 1.2e-2, 2.3e-3.  A transposed point factor (F Fᵀ instead of
+    FᵀF) stalls at 0.59 — checked when the pin was written."""
+    errs = [_curved_cavity_error(p, 0.04) for p in (2, 3, 4)]
+    assert errs[0] / errs[1] > 3.0 and errs[1] / errs[2] > 3.0 and errs[2] < 5e-3, errs
