@@ -86,7 +86,7 @@ typedef struct {
  *   DENSE:  the same operators assembled once per context into matrices (from the
  *           exact programs) and applied as block-sparse FP64 tensor-core GEMMs over
  *           tiles of elements (mma.sync m8n8k4), 3 launches per stage.
- *   HYBRID: (orders 7..10) the curl by the paper's recurrences as streamed
+ *   HYBRID: (orders 4..10) the curl by the paper's recurrences as streamed
  *           lane-per-element sweeps on the FP64 pipes, written to an
  *           internal ĉ buffer and added in the epilogue of the DENSE stage GEMM, which
  *           then applies only the lift; traces as in DENSE.  4 launches per stage.

@@ -677,12 +677,15 @@ dgm_status launch_pointmix(dgm_ctx *c, double *P, const double *K, cudaStream_t 
 
 dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st) {
   switch (c->p) {
+    case 4: return launch_curl_p4(c, Y, C, st);
+    case 5: return launch_curl_p5(c, Y, C, st);
+    case 6: return launch_curl_p6(c, Y, C, st);
     case 7: return launch_curl_p7(c, Y, C, st);
     case 8: return launch_curl_p8(c, Y, C, st);
     case 9: return launch_curl_p9(c, Y, C, st);
     case 10: return launch_curl_p10(c, Y, C, st);
   }
-  return set_err(c, DGM_EORDER, "streamed curl sweeps: orders 7..10");
+  return set_err(c, DGM_EORDER, "streamed curl sweeps: orders 4..10");
 }
 
 dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field) {

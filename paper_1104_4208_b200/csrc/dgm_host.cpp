@@ -638,14 +638,14 @@ dgm_status create_impl(dgm_ctx *c, const dgm_mesh *m, int order, const double *e
   // constant-table sweeps C4 5.79 vs 5.84 ms and C5 46.9 vs 48.3 ms per step against dense)
   int kind = o.engine;
   if (kind == DGM_ENGINE_AUTO) {
-    kind = p >= dgm::kCurlPmin ? DGM_ENGINE_HYBRID : p >= 6 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE;
+    kind = p >= dgm::kHybridAuto ? DGM_ENGINE_HYBRID : p >= 6 ? DGM_ENGINE_DENSE : DGM_ENGINE_SPARSE;
     if (const char *v = std::getenv("DGM_ENGINE"))
       kind = std::strcmp(v, "dense") == 0 ? DGM_ENGINE_DENSE
              : std::strcmp(v, "hybrid") == 0 && p >= dgm::kCurlPmin ? DGM_ENGINE_HYBRID
                                                                      : DGM_ENGINE_SPARSE;
   }
   if (kind == DGM_ENGINE_HYBRID && (p < dgm::kCurlPmin || p > dgm::kCurlPmax))
-    return dgm::set_err(c, DGM_EINVAL, "the hybrid engine covers orders 7..10");
+    return dgm::set_err(c, DGM_EINVAL, "the hybrid engine covers orders 4..10");
   c->engine = kind == DGM_ENGINE_SPARSE ? 0 : 1;
   c->sparse_curl = kind == DGM_ENGINE_HYBRID ? 1 : 0;
   // mixed orders E ∈ P^p, H ∈ P^{p-1}: dense engine, central/upwind

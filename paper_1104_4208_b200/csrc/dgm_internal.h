@@ -239,7 +239,11 @@ dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStre
 // curved elements: P[e][c Qk + i] <- Σ_l K[e][i][c,l] P[e][l Qk + i]
 dgm_status launch_pointmix(dgm_ctx *c, double *P, const double *K, cudaStream_t st);
 // streamed lane-per-element curl sweeps (dgm_curl.cuh, generated sweep/curl_p*.cu): ĉ of Y
-constexpr int kCurlPmin = 7, kCurlPmax = 10;
+constexpr int kCurlPmin = 4, kCurlPmax = 10;   // orders with generated curl sweeps (hybrid engine)
+constexpr int kHybridAuto = 7;                 // AUTO picks the hybrid engine from this order on
+dgm_status launch_curl_p4(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p5(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
+dgm_status launch_curl_p6(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
 dgm_status launch_curl(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
 dgm_status launch_curl_p7(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);
 dgm_status launch_curl_p8(dgm_ctx *c, const double *Y, double *C, cudaStream_t st);

@@ -69,7 +69,7 @@ def _rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-FULL = [(n, e) for n in ("C3", "C4", "C5") for e in ("sparse", "dense")] + [("C4", "hybrid"), ("C5", "hybrid")]
+FULL = [(n, e) for n in ("C3", "C4", "C5") for e in ("sparse", "dense")] + [("C3", "hybrid"), ("C4", "hybrid"), ("C5", "hybrid")]
 
 
 @pytest.mark.parametrize("name,engine", FULL)

@@ -46,8 +46,8 @@ ENGINES = ["sparse", "dense"]   # the paper's recurrences / the dense DMMA contr
 
 def engines(p):
     """Engines that run order p: the hybrid (streamed recurrence curl + DMMA lift and
-    traces) covers orders 7..10."""
-    return ENGINES + (["hybrid"] if 7 <= p <= 10 else [])
+    traces) covers orders 4..10."""
+    return ENGINES + (["hybrid"] if 4 <= p <= 10 else [])
 
 
 def combos(ps, extra=None):
@@ -317,7 +317,7 @@ def test_spectral_radius_vs_dense_eigen():
     assert not (c.dgm_energy(Ed, Hd) < 1e6 * w0)
 
 
-@pytest.mark.parametrize("engine,p", [("sparse", 5), ("dense", 5), ("hybrid", 7), ("hybrid", 10)])
+@pytest.mark.parametrize("engine,p", [("sparse", 5), ("dense", 5), ("hybrid", 4), ("hybrid", 7), ("hybrid", 10)])
 @pytest.mark.parametrize("flux", ["central", "upwind"])
 def test_single_tet_degenerate_mesh(engine, p, flux):
     """Degenerate case: one tetrahedron, all four faces PEC (every element tile and

@@ -48,7 +48,7 @@ CASES = [(p, (False,) * 3, 2) for p in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10)] + \
 
 
 def _eng(p):
-    return ["sparse", "dense"] + (["hybrid"] if p >= 7 else [])
+    return ["sparse", "dense"] + (["hybrid"] if p >= 4 else [])
 
 
 @pytest.mark.parametrize("p,periodic,n,engine", [c_ + (e_,) for c_ in CASES for e_ in _eng(c_[0])])

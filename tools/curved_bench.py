@@ -5,7 +5,9 @@ the flat path the diagonal inverse mass.  Paper, for context (PAPER.md:536-576,
 Table 1, one Xeon 5160 core, 2078 tets, µs per step and 6 DOFs): flat / curved
 p=2 0.58/2.54, p=4 0.79/1.79, p=6 1.24/2.17, p=8 1.53/2.67, p=10 1.74/3.04.
 usage: python tools/curved_bench.py [n] [p,p,...]"""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch

@@ -4,7 +4,7 @@ usage: python tools/sass_histogram.py [lib] > profiles/rNN_sass_histogram.txt
 
 For every kernel in `cuobjdump -sass` it counts the instructions that prove which pipes
 and copy engines the code uses: DMMA (FP64 tensor core, mma.sync m8n8k4), DFMA/DADD/DMUL
-(FP64 pipe), LDGSTS (cp.async), UBLKCP (cp.async.bulk), UTMALDG (tensor-map TMA), LDS/STS,
+(FP64 pipe), LDGSTS (cp.async), LDL/STL (register spills), LDCU (uniform constant loads), UBLKCP (cp.async.bulk), UTMALDG (tensor-map TMA), LDS/STS,
 LDG/STG (with vector widths), BAR/SYNCS (barriers, mbarriers), and the total.
 """
 import collections
@@ -12,7 +12,7 @@ import re
 import subprocess
 import sys
 
-KEYS = ["DMMA", "DFMA", "DADD", "DMUL", "LDGSTS", "UBLKCP", "UTMALDG", "LDS", "STS", "LDG", "STG", "LDC", "ULDC",
+KEYS = ["DMMA", "DFMA", "DADD", "DMUL", "LDGSTS", "UBLKCP", "UTMALDG", "LDS", "STS", "LDG", "STG", "LDL", "STL", "LDC", "LDCU", "ULDC",
         "UMOV", "BAR", "SYNCS", "SHFL"]
 
 
