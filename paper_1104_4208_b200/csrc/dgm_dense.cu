@@ -598,6 +598,32 @@ dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY,
     g.rawNk = Nk;
     dgm_status s = gemm_go<EPI_STAGE>(c, g, st);
     if (s != DGM_OK) return s;
+    if (D.use_sumfact) {   // sum-factorised point transforms, O(p⁴)
+      SumfactArgs sa{};
+      sa.AC = D.AC;
+      sa.acld = 3 * Nk;
+      sa.acNk = Nk;
+      sa.Pc = D.sf_tab + D.sf_pc;
+      sa.Bb = D.sf_tab + D.sf_bb;
+      sa.Ca = D.sf_tab + D.sf_ca;
+      sa.inv_norms = D.sf_tab + D.sf_in;
+      sa.modes = D.sf_modes;
+      sa.pairs = D.sf_pairs;
+      sa.K = c->curved ? (a.stage == STAGE_E ? D.KE : D.KH) : nullptr;
+      sa.SW = a.stage == STAGE_E ? D.SWe : D.SWm;
+      sa.Qk = Qk;
+      sa.geo = c->d_geo;
+      sa.X = a.X;
+      sa.dX = a.dX;
+      sa.dt = a.dt;
+      sa.n_tet = c->n_tet;
+      sa.LD = c->LD;
+      sa.stageE = a.stage == STAGE_E;
+      sa.out_mode = a.out_mode;
+      if ((s = launch_sumfact(c, sa, st)) != DGM_OK) return s;
+      if (a.out_mode == OUT_UPDATE && trOut) return launch_dense_traces(c, a.X, trOut, st, v);
+      return DGM_OK;
+    }
     GemmArgs f{};
     f.p0 = f.p1 = D.AC;
     f.ld0 = f.ld1 = 3 * Nk;

@@ -559,6 +559,53 @@ dgm_status dense_build(dgm_ctx *c, const HostProgSet &hs) {
                (!c->curved || (up((void **)&D.KE, c->h_ke.data(), c->h_ke.size() * 8) &&
                                up((void **)&D.KH, c->h_kh.data(), c->h_kh.size() * 8)));
     if (!okm) return dgm::set_err(c, DGM_ENOMEM, "dense_build: material-point operators");
+    // sum-factorised transforms: the 1D factors of φ_ijk at the
+    // collapsed rule's coordinates a (x-direction, weight (2,0)), b ((1,0)), c ((0,0)):
+    //   Pc[i][γ] = P_i(c_γ),  Bb[i][j][β] = ((1-b_β)/2)^i P_j^{(2i+1,0)}(b_β),
+    //   Ca[t][k][α] = ((1-a_α)/2)^t P_k^{(2t+2,0)}(a_α)
+    {
+      const int p = c->p, P1 = p + 1, q = p + 2;
+      std::vector<double> qa, wa, qb, wb, qc, wc;
+      gauss_jacobi(q, 2.0, qa, wa);
+      gauss_jacobi(q, 1.0, qb, wb);
+      gauss_jacobi(q, 0.0, qc, wc);
+      D.sf_pc = 0;
+      D.sf_bb = P1 * q;
+      D.sf_ca = D.sf_bb + P1 * P1 * q;
+      D.sf_in = D.sf_ca + P1 * P1 * q;
+      std::vector<double> tab((size_t)D.sf_in + N, 0.0);
+      double Pv, d;
+      for (int i = 0; i <= p; ++i)
+        for (int g = 0; g < q; ++g) {
+          jacobi_pd(i, 0.0, qc[g], Pv, d);
+          tab[D.sf_pc + i * q + g] = Pv;
+        }
+      for (int i = 0; i <= p; ++i)
+        for (int j = 0; i + j <= p; ++j)
+          for (int g = 0; g < q; ++g) {
+            jacobi_pd(j, 2.0 * i + 1.0, qb[g], Pv, d);
+            tab[D.sf_bb + (i * P1 + j) * q + g] = std::pow(0.5 * (1.0 - qb[g]), i) * Pv;
+          }
+      for (int t = 0; t <= p; ++t)
+        for (int k = 0; t + k <= p; ++k)
+          for (int g = 0; g < q; ++g) {
+            jacobi_pd(k, 2.0 * t + 2.0, qa[g], Pv, d);
+            tab[D.sf_ca + (t * P1 + k) * q + g] = std::pow(0.5 * (1.0 - qa[g]), t) * Pv;
+          }
+      std::vector<int3> modes;
+      for (int n = 0; n <= p; ++n)
+        for (int i = 0; i <= n; ++i)
+          for (int j = 0; j <= n - i; ++j) modes.push_back(make_int3(i, j, n - i - j));
+      for (int b = 0; b < N; ++b) tab[D.sf_in + b] = 1.0 / hs.norms[b];
+      std::vector<int2> pairs;
+      for (int i = 0; i <= p; ++i)
+        for (int j = 0; i + j <= p; ++j) pairs.push_back(make_int2(i, j));
+      if (!up((void **)&D.sf_tab, tab.data(), tab.size() * 8) ||
+          !up((void **)&D.sf_modes, modes.data(), modes.size() * sizeof(int3)) ||
+          !up((void **)&D.sf_pairs, pairs.data(), pairs.size() * sizeof(int2)))
+        return dgm::set_err(c, DGM_ENOMEM, "dense_build: sum-factorisation tables");
+      if (const char *v = std::getenv("DGM_POINT_GEMM")) D.use_sumfact = std::atoi(v) == 0;
+    }
     D.ncf = ncf;
     CUDA_TRY(c, cudaMalloc(&D.AC, sizeof(double) * 3 * (size_t)Nk * (size_t)(n_or1(c))));
     CUDA_TRY(c, cudaMemset(D.AC, 0, sizeof(double) * 3 * (size_t)Nk * (size_t)(n_or1(c))));
@@ -589,7 +636,8 @@ void free_ctx(dgm_ctx *c) {
   cudaFree(c->dense.Cc);
   for (void *q : {(void *)c->dense.Bf, (void *)c->dense.Bb, (void *)c->dense.ktlf, (void *)c->dense.ktofff,
                   (void *)c->dense.ktlb, (void *)c->dense.ktoffb, (void *)c->dense.SWe, (void *)c->dense.SWm,
-                  (void *)c->dense.AC, (void *)c->dense.P, (void *)c->dense.KE, (void *)c->dense.KH})
+                  (void *)c->dense.AC, (void *)c->dense.P, (void *)c->dense.KE, (void *)c->dense.KH,
+                  (void *)c->dense.sf_tab, (void *)c->dense.sf_modes, (void *)c->dense.sf_pairs})
     cudaFree(q);
   cudaFree(c->d_stream);
   cudaFree(c->d_geo);

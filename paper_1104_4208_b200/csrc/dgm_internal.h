@@ -107,6 +107,13 @@ struct DenseOps {
   double *Bf = nullptr, *Bb = nullptr, *SWe = nullptr, *SWm = nullptr, *AC = nullptr, *P = nullptr;
   // curved elements: per point K_i = ŵ_i F(ξ_i)ᵀF(ξ_i) / (m det F(ξ_i)), [n][Qk][6] (E: ε, H: μ)
   double *KE = nullptr, *KH = nullptr;
+  // sum-factorised point transforms (dgm_sumfact.cu): 1D tables Pc, Bb, Ca, 1/‖φ‖², and
+  // the (i, j, k) of every graded mode
+  double *sf_tab = nullptr;
+  int3 *sf_modes = nullptr;
+  int2 *sf_pairs = nullptr;
+  int sf_pc = 0, sf_bb = 0, sf_ca = 0, sf_in = 0;   // offsets into sf_tab
+  int use_sumfact = 1;                               // 0: dense Φ GEMMs (DGM_POINT_GEMM=1)
   uint64_t *ktlf = nullptr, *ktlb = nullptr;
   int32_t *ktofff = nullptr, *ktoffb = nullptr;
   int ncf = 0;
@@ -114,6 +121,7 @@ struct DenseOps {
   double *Cc = nullptr;
   int ldc = 0;
 };
+
 
 struct DevProgs {
   DevProg curl;
@@ -127,6 +135,24 @@ struct DevProgs {
 struct Geo {
   double g[6];
   double detF, inv_eps, inv_mu, Z;
+};
+
+// sum-factorised reverse numerical integration (dgm_sumfact.cu)
+struct SumfactArgs {
+  const double *AC;       // residual after the reference mass, [n][acld], component c at c*acNk
+  int64_t acld;
+  int acNk;
+  const double *Pc, *Bb, *Ca, *inv_norms;
+  const int3 *modes;
+  const int2 *pairs;      // the (i, j) with i + j <= p, i outer
+  const double *K;        // curved: [n][Qk][6] point factors (else null)
+  const double *SW;       // flat variable materials: [n][Qk] ŵ_i / m(x_i)
+  int Qk;
+  const Geo *geo;
+  double *X, *dX;
+  double dt;
+  int64_t n_tet;
+  int LD, stageE, out_mode;
 };
 
 enum OutMode { OUT_UPDATE = 0, OUT_WRITE = 1, OUT_ACCUM = 2 };
@@ -236,6 +262,7 @@ dgm_status launch_seed(dgm_ctx *c, double *X, uint64_t seed, cudaStream_t st);
 // dense-contraction engine (dgm_dense.cu), all orders
 dgm_status launch_dense_stage(dgm_ctx *c, const StageArgs &a, const double *trY, double *trOut, cudaStream_t st);
 dgm_status launch_dense_traces(dgm_ctx *c, const double *X, double *tr, cudaStream_t st, int field);
+dgm_status launch_sumfact(dgm_ctx *c, const SumfactArgs &a, cudaStream_t st);
 // curved elements: P[e][c Qk + i] <- Σ_l K[e][i][c,l] P[e][l Qk + i]
 dgm_status launch_pointmix(dgm_ctx *c, double *P, const double *K, cudaStream_t st);
 // streamed lane-per-element curl sweeps (dgm_curl.cuh, generated sweep/curl_p*.cu): ĉ of Y

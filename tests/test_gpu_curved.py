@@ -120,3 +120,19 @@ def test_curved_rejects_bad_input():
         c.dgm_energy(c.empty_field(), c.empty_field())
     with pytest.raises(ValueError):
         Context(cm.xyz, cm.tet, 2, edge_nodes=en[:, :5])
+
+
+@pytest.mark.parametrize("p", [4, 9])
+def test_curved_point_gemm_path_parity(p, monkeypatch):
+    """Same operator through the dense Φ point GEMMs + pointmix kernel (DGM_POINT_GEMM=1)."""
+    monkeypatch.setenv("DGM_POINT_GEMM", "1")
+    m, rep, c, C = _case(p, (True,) * 3, 3)
+    rng = np.random.default_rng(p)
+    E = rng.standard_normal((3, m.n_tet, c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N))
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    dE, dH = c.empty_field(), c.empty_field()
+    c.dgm_apply_curl(Ed, Hd, dE, dH)
+    c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
+    assert _rel(c.to_host(dE), C.dE(E, H)) <= 1e-12
+    assert _rel(c.to_host(dH), C.dH(E, H)) <= 1e-12

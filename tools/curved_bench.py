@@ -40,6 +40,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 ps = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,4,6,8,10").split(",")]
 m = di.kuhn_mesh(n, periodic=(True, True, True), jitter=0.1, seed=1)
 cm, en = di.curved_mesh(m, 0.03)
+point_gemm = os.environ.get("DGM_POINT_GEMM", "0") != "0"
+print(f"point transforms: {'dense Φ GEMMs' if point_gemm else 'sum-factorised'}", flush=True)
 for p in ps:
     c = Context(m.xyz, m.tet, p, rep=m.rep)
     tf = time_step(c, p, m.n_tet)

@@ -1,5 +1,8 @@
 """Throughput of intra-element variable materials (reverse numerical integration,
 dense engine) against constant-per-element materials on the same meshes."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
