@@ -1,7 +1,7 @@
 // Streamed-table high-order stage kernels (p > kLanePmax), sm_100a FP64.
 //
-// Same per-element algorithm as stage2_kernel (dgm_kernels.cu; SURVEY.md §8(a)
-// S1-S6): recurrence curl, flux on the trace-buffer
+// The per-element algorithm of the sparse engine (as in the
+// lane-pair kernels of dgm_lane.cu): recurrence curl, flux on the trace-buffer
 // traces, staged sum-factorised lift, inverse mass with G'
 // (PAPER.md:465-476), symplectic-Euler update, traces of the
 // updated field.
