@@ -129,3 +129,46 @@ def test_c3_upwind_energy_decays():
     c.dgm_step(Ed, Hd, 2e-4, 10)
     w1 = c.dgm_energy(Ed, Hd)
     assert np.isfinite(w1) and w1 <= w0 * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("engine", ["dense", "hybrid"])
+def test_c3_mesh_stabilized_flux_every_element(engine):
+    """NEXT-1 at full size: the stabilised central flux with face unknowns H^F
+     on the C3 mesh (196,608 tets, 399,360 faces, p = 6, ε per
+    element, PEC): the time derivatives (Ė, Ḣ, Ḣ^F) of every element and face, and one
+    (H, H^F, E) leapfrog step, against oracle.tier_b.TierBStab (≤ 1e-12 each)."""
+    import torch
+    from paper_1104_4208_b200 import Context
+    from oracle.tier_b import TierBStab, symplectic_euler_stab
+    m = di.config_mesh("C3")
+    eps, mu = di.config_materials("C3", m.n_tet)
+    p = 6
+    c = Context(m.xyz, m.tet, p, eps=eps, mu=mu, flux="stabilized", engine=engine)
+    B = TierBStab(m.xyz, m.tet, None, p, eps, mu)
+    nf, _ = c.dgm_faces()
+    assert nf == B.n_faces
+    rng = np.random.default_rng(3003)
+    scale = 1.0 / (1.0 + di.mode_degrees(p)) ** 2
+    E = rng.standard_normal((3, m.n_tet, c.N)) * scale
+    H = rng.standard_normal((3, m.n_tet, c.N)) * scale
+    NF = (p + 1) * (p + 2) // 2
+    HF = rng.standard_normal((nf, 2, NF)) / NF
+
+    def dev(X):
+        D = c.empty_field()
+        D[:, :, :c.N] = torch.as_tensor(X, device="cuda")
+        return D
+    Ed, Hd = dev(E), dev(H)
+    HFd = torch.as_tensor(HF, device="cuda").contiguous()
+    dE, dH = c.empty_field(), c.empty_field()
+    dHF = torch.empty_like(HFd)
+    c.dgm_rhs_sc(Ed, Hd, HFd, dE, dH, dHF)
+    assert _rel(dE[:, :, :c.N].cpu().numpy(), B.dE(E, H, HF)) <= TOL
+    assert _rel(dH[:, :, :c.N].cpu().numpy(), B.dH(E, H)) <= TOL
+    assert _rel(dHF.cpu().numpy(), B.dHF(E)) <= TOL
+    dt = 1e-4
+    c.dgm_step_sc(Ed, Hd, HFd, dt, 1)
+    E1, H1, HF1 = symplectic_euler_stab(B, E, H, HF, dt, 1)
+    assert _rel(Ed[:, :, :c.N].cpu().numpy(), E1) <= TOL
+    assert _rel(Hd[:, :, :c.N].cpu().numpy(), H1) <= TOL
+    assert _rel(HFd.cpu().numpy(), HF1) <= TOL
