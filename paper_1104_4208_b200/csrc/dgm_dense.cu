@@ -246,6 +246,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB) gemm_kernel(GemmArgs g) 
           const double *px = g.X + (q % 3) * cs + e * g.LD + 32 * NH * nt;
 #pragma unroll
           for (int l = 0; l < 2 * NH; ++l) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(px + 16 * l));
+          if (g.cc && 32 * NH * nt < g.ncc) {   // hybrid: the tile's block of the sweeps' ĉ too
+            const double *pc = g.cc + (q % 3) * g.ccs + e * g.ldc + 32 * NH * nt;
+#pragma unroll
+            for (int l = 0; l < 2 * NH; ++l) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pc + 16 * l));
+          }
         }
       }
     }
