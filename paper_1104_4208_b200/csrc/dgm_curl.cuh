@@ -29,6 +29,9 @@
 // lockstep barrier instead of the pair barrier changes neither.  The sweeps sit at
 // 8-10% of the FP64 pipe: 255 registers (a two-degree-level window of u per lane) leave
 // two warps per scheduler, and every instruction-line fetch or constant load is exposed.
+// Warp pairs per CTA (DGM_CURL_NPAIR, same 8 warps per SM): 4 pairs 6.71 ms, 2 pairs
+// 9.90, 1 pair 18.5 — CTAs on one SM then run different output components, i.e. more
+// distinct instruction streams and constant tables per SM.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -44,7 +47,10 @@ constexpr int SLOT = CH * CS;     // doubles per output slot
 constexpr int RS = 18;            // input slot row stride (16 modes + pad, 16-byte aligned rows)
 constexpr int SLOT_IN = 32 * RS;  // doubles per input slot ([element][RS])
 constexpr int RIN = 3, ROUT = 2;  // ring slots
-constexpr int NPAIR = 4;          // warp pairs per CTA
+#ifndef DGM_CURL_NPAIR
+#define DGM_CURL_NPAIR 4
+#endif
+constexpr int NPAIR = DGM_CURL_NPAIR;   // warp pairs per CTA
 constexpr int WARP_SMEM = RIN * SLOT_IN + ROUT * SLOT;   // doubles of ring per warp
 
 // a 64-bit immediate operand (the sweeps' coefficients): volatile so ptxas keeps it an
