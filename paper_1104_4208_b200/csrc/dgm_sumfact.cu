@@ -24,6 +24,7 @@
 // equation and the update X += dt Ẋ (or writes / accumulates dX).
 // The 1D tables (host-built, dgm_host.cpp: sumfact_tables) are read through L1.
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "dgm_internal.h"
@@ -42,6 +43,9 @@ struct SF {
   static constexpr int EL = 3 * N + W_SZ + 3 * U_SZ;               // doubles per element
   static constexpr int EB = 256 / (Q1 * Q1) > 0 ? 256 / (Q1 * Q1) : 1;   // elements per CTA
   static constexpr int SMEM = 8 * EB * EL;
+  // measured on a 10,368-tet curved cube (profiles/r02_sumfact_minb.txt): 3 CTAs per SM
+  // (80 registers) is faster for p <= 5 and p = 10, 2 (128 registers) for p = 6..9
+  static constexpr int MINB_DEFAULT = (P >= 6 && P <= 9) ? 2 : 3;
 };
 
 __device__ __forceinline__ int mode_index(int i, int j, int k) {
@@ -49,8 +53,8 @@ __device__ __forceinline__ int mode_index(int i, int j, int k) {
   return n * (n + 1) * (n + 2) / 6 + i * (n + 1) - i * (i - 1) / 2 + j;
 }
 
-template <int P>
-__global__ void __launch_bounds__(256, 2) sumfact_kernel(SumfactArgs a) {
+template <int P, int MINB>
+__global__ void __launch_bounds__(256, MINB) sumfact_kernel(SumfactArgs a) {
   using S = SF<P>;
   constexpr int Q1 = S::Q1, QS = S::QS, N = S::N, NP = S::NP, P1 = P + 1, EB = S::EB, EL = S::EL;
   extern __shared__ __align__(16) double sm[];
@@ -108,66 +112,74 @@ __global__ void __launch_bounds__(256, 2) sumfact_kernel(SumfactArgs a) {
       }
       __syncthreads();
     }
-    // ---- C, the point factor and Cᵀ fused per column (α, β): thread (α, β) holds the
-    // column's point values of the three components in registers (point index
-    // (α q + β) q + γ, the host rule's order) and writes U'_c[i][α][β] in place
-    for (int o = tid; o < nel * Q1 * Q1; o += T) {
-      const int l = o / (Q1 * Q1), col = o - l * Q1 * Q1, al = col / Q1, be = col - al * Q1;
-      double *U = UU(l);
-      double f[3][Q1];
+    // ---- C, the point factor and Cᵀ fused per column (α, β): the two lanes of a pair
+    // take the column's first and second half of γ, hold those point values of the three
+    // components in registers (point index (α q + β) q + γ, the host rule's order), and
+    // combine their Cᵀ partial sums with one shuffle; U'_c[i][α][β] is written in place
+    {
+      constexpr int G2 = (Q1 + 1) / 2;
+      const int count = nel * Q1 * Q1 * 2;
+      for (int ob = 0; ob < count; ob += T) {   // uniform trip count: the shuffles need every lane
+        const int o = ob + tid;
+        const bool act = o < count;
+        const int oc = act ? o >> 1 : 0, h = o & 1;
+        const int l = oc / (Q1 * Q1), col = oc - l * Q1 * Q1, al = col / Q1, be = col - al * Q1;
+        double *U = UU(l);
+        const int g0 = h * G2;
+        double f[3][G2];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int g = 0; g < Q1; ++g) f[c][g] = 0.0;
-      for (int i = 0; i <= P; ++i) {
-        const int ui = (i * Q1 + al) * QS + be;
-        const double u0 = U[ui], u1 = U[S::U_SZ + ui], u2 = U[2 * S::U_SZ + ui];
+          for (int g = 0; g < G2; ++g) f[c][g] = 0.0;
+        for (int i = 0; i <= P; ++i) {
+          const int ui = (i * Q1 + al) * QS + be;
+          const double u0 = U[ui], u1 = U[S::U_SZ + ui], u2 = U[2 * S::U_SZ + ui];
 #pragma unroll
-        for (int g = 0; g < Q1; ++g) {
-          const double pc = __ldg(Pc + i * Q1 + g);
-          f[0][g] = fma(pc, u0, f[0][g]);
-          f[1][g] = fma(pc, u1, f[1][g]);
-          f[2][g] = fma(pc, u2, f[2][g]);
+          for (int g = 0; g < G2; ++g)
+            if (g0 + g < Q1) {
+              const double pc = __ldg(Pc + i * Q1 + g0 + g);
+              f[0][g] = fma(pc, u0, f[0][g]);
+              f[1][g] = fma(pc, u1, f[1][g]);
+              f[2][g] = fma(pc, u2, f[2][g]);
+            }
         }
-      }
-      const int64_t pt0 = (e0 + l) * (int64_t)a.Qk + (int64_t)col * Q1;
+        const int64_t pt0 = (e0 + l) * (int64_t)a.Qk + (int64_t)col * Q1 + g0;
 #pragma unroll
-      for (int g = 0; g < Q1; ++g) {
-        if (a.K) {
-          const double *k = a.K + (pt0 + g) * 6;
-          const double v0 = f[0][g], v1 = f[1][g], v2 = f[2][g];
-          f[0][g] = k[0] * v0 + k[1] * v1 + k[2] * v2;
-          f[1][g] = k[1] * v0 + k[3] * v1 + k[4] * v2;
-          f[2][g] = k[2] * v0 + k[4] * v1 + k[5] * v2;
-        } else {
-          const double w = a.SW[pt0 + g];
-          f[0][g] *= w;
-          f[1][g] *= w;
-          f[2][g] *= w;
-        }
-      }
-      for (int i = 0; i <= P; ++i) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
-#pragma unroll
-        for (int g = 0; g < Q1; g += 2) {
-          const double pc = __ldg(Pc + i * Q1 + g);
-          s0 = fma(pc, f[0][g], s0);
-          s1 = fma(pc, f[1][g], s1);
-          s2 = fma(pc, f[2][g], s2);
-          if (g + 1 < Q1) {
-            const double pd = __ldg(Pc + i * Q1 + g + 1);
-            r0 = fma(pd, f[0][g + 1], r0);
-            r1 = fma(pd, f[1][g + 1], r1);
-            r2 = fma(pd, f[2][g + 1], r2);
+        for (int g = 0; g < G2; ++g) {
+          if (!act || g0 + g >= Q1) continue;
+          if (a.K) {
+            const double *k = a.K + (pt0 + g) * 6;
+            const double v0 = f[0][g], v1 = f[1][g], v2 = f[2][g];
+            f[0][g] = k[0] * v0 + k[1] * v1 + k[2] * v2;
+            f[1][g] = k[1] * v0 + k[3] * v1 + k[4] * v2;
+            f[2][g] = k[2] * v0 + k[4] * v1 + k[5] * v2;
+          } else {
+            const double w = a.SW[pt0 + g];
+            f[0][g] *= w;
+            f[1][g] *= w;
+            f[2][g] *= w;
           }
         }
-        s0 += r0;
-        s1 += r1;
-        s2 += r2;
-        const int ui = (i * Q1 + al) * QS + be;
-        U[ui] = s0;
-        U[S::U_SZ + ui] = s1;
-        U[2 * S::U_SZ + ui] = s2;
+        for (int i = 0; i <= P; ++i) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int g = 0; g < G2; ++g)
+            if (g0 + g < Q1) {
+              const double pc = __ldg(Pc + i * Q1 + g0 + g);
+              s0 = fma(pc, f[0][g], s0);
+              s1 = fma(pc, f[1][g], s1);
+              s2 = fma(pc, f[2][g], s2);
+            }
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+          if (act && h == (i & 1)) {   // the pair splits the stores
+            const int ui = (i * Q1 + al) * QS + be;
+            U[ui] = s0;
+            U[S::U_SZ + ui] = s1;
+            U[2 * S::U_SZ + ui] = s2;
+          }
+        }
       }
     }
     __syncthreads();
@@ -241,23 +253,36 @@ __global__ void __launch_bounds__(256, 2) sumfact_kernel(SumfactArgs a) {
   }
 }
 
-template <int P>
-dgm_status go(dgm_ctx *c, const SumfactArgs &a, cudaStream_t st) {
+template <int P, int MINB>
+dgm_status go_b(dgm_ctx *c, const SumfactArgs &a, cudaStream_t st) {
   constexpr int smem = SF<P>::SMEM;
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(sumfact_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sumfact_kernel<P>, 256, smem);
+    cudaFuncSetAttribute(sumfact_kernel<P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sumfact_kernel<P, MINB>, 256, smem);
     if (occ < 1) occ = 1;
   }
   const int64_t groups = (c->n_tet + SF<P>::EB - 1) / SF<P>::EB;
   int64_t grid = (int64_t)c->sms * occ;
   if (grid > groups) grid = groups;
   if (grid < 1) return DGM_OK;
-  sumfact_kernel<P><<<(unsigned)grid, 256, smem, st>>>(a);
+  sumfact_kernel<P, MINB><<<(unsigned)grid, 256, smem, st>>>(a);
   c->launches++;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("sumfact_kernel: ") + cudaGetErrorString(e));
+}
+
+// CTAs per SM the register allocation targets (launch bounds): 3 (80 registers) or 2
+// (128); DGM_SF_MINB=2|3 overrides for measurements
+template <int P>
+dgm_status go(dgm_ctx *c, const SumfactArgs &a, cudaStream_t st) {
+  static int minb = 0;
+  if (!minb) {
+    minb = SF<P>::MINB_DEFAULT;
+    if (const char *v = std::getenv("DGM_SF_MINB"))
+      if (std::atoi(v) == 2 || std::atoi(v) == 3) minb = std::atoi(v);
+  }
+  return minb == 2 ? go_b<P, 2>(c, a, st) : go_b<P, 3>(c, a, st);
 }
 
 }  // namespace
