@@ -153,3 +153,70 @@ def test_curved_cavity_mode_converges_in_p():
     FᵀF) stalls at 0.59 — checked when the pin was written."""
     errs = [_curved_cavity_error(p, 0.04) for p in (2, 3, 4)]
     assert errs[0] / errs[1] > 3.0 and errs[1] / errs[2] > 3.0 and errs[2] < 5e-3, errs
+
+
+def test_covariant_identities_hold_pointwise_on_curved_elements():
+    """The curved oracle (and the library) keep the flat path's geometry-free curl and
+    face terms; this pins that reading (G19) by direct physical differentiation on a
+    curved element, independently of the oracle's operator code:
+      volume: |det F| H·curl_x e = sign(det F) Ĥ·curl̂ ê at every point, with H = F⁻ᵀĤ,
+              e = F⁻ᵀê and curl_x from finite differences of x̂ ↦ F(x̂)⁻ᵀê(x̂) chained with
+              F⁻¹ (PAPER.md:367-370, A.6 of the survey for affine maps);
+      faces:  (ν_out × a)·e |F t̂₁ × F t̂₂| = (-1)^f sign(det F) (a₁e₂ - a₂e₁), a_k = â·t̂_k,
+              ν_out oriented by the cofactor normal F⁻ᵀ n̂_f."""
+    from oracle.basis import phi, face_map, face_tangents
+    from oracle.jacobi import tet_rule, tri_rule
+    m = di.kuhn_mesh(2, jitter=0.1, seed=3)
+    cm, en = di.curved_mesh(m, 0.04)
+    p = 2
+    rng = np.random.default_rng(5)
+    N = (p + 1) * (p + 2) * (p + 3) // 6
+    Hc, ec = rng.standard_normal((3, N)), rng.standard_normal((3, N))
+    nodes_all = p2_nodes(cm.xyz, cm.tet, en)
+
+    def ref_field(c, pts):
+        return (phi(p, pts).T @ c.T)                                   # [Q, 3]
+
+    def phys_field(c, nodes, pts):
+        F = p2_jacobian(nodes, pts)[0]
+        return np.einsum("qji,qj->qi", np.linalg.inv(F), ref_field(c, pts)), F   # F⁻ᵀ v
+
+    for T in (3, 17, 40):
+        nodes = nodes_all[T:T + 1]
+        pts, _ = tet_rule(4)
+        eh, F = phys_field(ec, nodes, pts)
+        Hh, _ = phys_field(Hc, nodes, pts)
+        det = np.linalg.det(F)
+        sgn = np.sign(det[0])
+        assert np.all(np.sign(det) == sgn)
+        h = 1e-5
+        J = np.empty((pts.shape[0], 3, 3))                             # ∂(F⁻ᵀê)/∂x̂_j
+        for j in range(3):
+            d = np.zeros(3)
+            d[j] = h
+            J[:, :, j] = (phys_field(ec, nodes, pts + d)[0] - phys_field(ec, nodes, pts - d)[0]) / (2 * h)
+        Dx = np.einsum("qij,qjk->qik", J, np.linalg.inv(F))           # ∂e/∂x
+        curl = np.stack([Dx[:, 2, 1] - Dx[:, 1, 2], Dx[:, 0, 2] - Dx[:, 2, 0], Dx[:, 1, 0] - Dx[:, 0, 1]], axis=1)
+        lhs = np.abs(det) * np.einsum("qi,qi->q", Hh, curl)
+        V, G = phi(p, pts, grad=True)
+        ge = np.einsum("cn,dnq->qcd", ec, G)                           # ∂ê_c/∂x̂_d
+        curl_ref = np.stack([ge[:, 2, 1] - ge[:, 1, 2], ge[:, 0, 2] - ge[:, 2, 0], ge[:, 1, 0] - ge[:, 0, 1]], axis=1)
+        rhs = sgn * np.einsum("qi,qi->q", ref_field(Hc, pts), curl_ref)
+        assert np.abs(lhs - rhs).max() <= 1e-7 * np.abs(rhs).max()
+        # faces
+        uv, _ = tri_rule(4)
+        nref = [np.array([1.0, 1.0, 1.0]), np.array([-1.0, 0, 0]), np.array([0, -1.0, 0]), np.array([0, 0, -1.0])]
+        for f in range(4):
+            xf = face_map(f, uv)
+            t1, t2 = face_tangents(f)
+            Ff = p2_jacobian(nodes, xf)[0]
+            nvec = np.cross(Ff @ t1, Ff @ t2)                           # F t̂1 × F t̂2 per point
+            cof = np.einsum("qji,j->qi", np.linalg.inv(Ff), nref[f])   # F⁻ᵀ n̂_f (outward)
+            s_out = np.sign(np.einsum("qi,qi->q", nvec, cof))
+            a_phys, _ = phys_field(Hc, nodes, xf)
+            e_phys, _ = phys_field(ec, nodes, xf)
+            lhs_f = s_out * np.einsum("qi,qi->q", nvec, np.cross(a_phys, e_phys))   # (ν×a)·e |n|
+            ah, eh_ = ref_field(Hc, xf), ref_field(ec, xf)
+            a1, a2, e1, e2 = ah @ t1, ah @ t2, eh_ @ t1, eh_ @ t2
+            rhs_f = (-1.0) ** f * sgn * (a1 * e2 - a2 * e1)
+            assert np.abs(lhs_f - rhs_f).max() <= 1e-12 * np.abs(rhs_f).max(), (T, f)
