@@ -45,7 +45,8 @@ def _case(p, periodic, n, delta=0.03, seed=3, materials="element"):
 
 
 CASES = [((False,) * 3, 2), ((True,) * 3, 3), ((False, True, True), (2, 3, 3))]
-APPLY = [(p, pc, n) for p in (1, 2, 3, 5, 6) for pc, n in CASES] + [(7, (False,) * 3, 2), (8, (True,) * 3, 3),
+APPLY = [(p, pc, n) for p in (1, 2, 3, 5, 6) for pc, n in CASES] + [(4, (True,) * 3, 3), (7, (False,) * 3, 2),
+                                                                   (8, (True,) * 3, 3), (9, (False, True, True), (2, 3, 3)),
                                                                    (10, (False,) * 3, 2)]
 
 
@@ -136,3 +137,32 @@ def test_curved_point_gemm_path_parity(p, monkeypatch):
     c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
     assert _rel(c.to_host(dE), C.dE(E, H)) <= 1e-12
     assert _rel(c.to_host(dH), C.dH(E, H)) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [3, 8])
+def test_single_curved_tet(p):
+    """Degenerate case: one curved tetrahedron, all faces PEC (a 1-element group in the
+    sum-factorised kernel and a ragged GEMM tile): apply and 20 steps vs the oracle."""
+    from paper_1104_4208_b200 import Context
+    xyz = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], dtype=float)
+    tet = np.array([[0, 1, 2, 3]], dtype=np.int32)
+    X = xyz[tet[0]]
+    en = np.stack([0.5 * (X[a] + X[b]) for a, b in EDGES])[None].copy()
+    en[0, 5] += np.array([0.05, 0.04, 0.0])   # bend edge (2,3)
+    en[0, 0] += np.array([0.0, -0.03, 0.02])  # and edge (0,1)
+    c = Context(xyz, tet, p, eps=2.0, mu=1.5, edge_nodes=en)
+    C = curved_oracle(xyz, tet, None, p, en, 2.0, 1.5)
+    rng = np.random.default_rng(p)
+    E = rng.standard_normal((3, 1, c.N)) / (1 + np.arange(c.N))
+    H = rng.standard_normal((3, 1, c.N)) / (1 + np.arange(c.N))
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    dE, dH = c.empty_field(), c.empty_field()
+    c.dgm_apply_curl(Ed, Hd, dE, dH)
+    c.dgm_apply_flux(Ed, Hd, dE, dH, accumulate=True)
+    assert _rel(c.to_host(dE), C.dE(E, H)) <= 1e-12
+    assert _rel(c.to_host(dH), C.dH(E, H)) <= 1e-12
+    dt = 0.01 / (p + 1) ** 2
+    c.dgm_step(Ed, Hd, dt, 20)
+    Er, Hr, _ = symplectic_euler(C, E, H, dt, 20)
+    assert _rel(c.to_host(Ed), Er) <= 1e-10
+    assert _rel(c.to_host(Hd), Hr) <= 1e-10
