@@ -512,14 +512,18 @@ dgm_status gemm_go_c(dgm_ctx *c, const GemmArgs &g0, cudaStream_t st) {
   return e == cudaSuccess ? DGM_OK : set_err(c, DGM_ECUDA, std::string("gemm_kernel: ") + cudaGetErrorString(e));
 }
 
-int dense_cfg() {
-  const char *v = std::getenv("DGM_DENSE_CFG");
+// CTA tile configuration (measurement overrides): DGM_DENSE_CFG for every GEMM,
+// DGM_STAGE_CFG / DGM_TRACE_CFG per GEMM type (0: 64x3 stages, the default; 1: 64x4;
+// 2: 128x3; 3: 32x4)
+int dense_cfg(int epi) {
+  const char *v = std::getenv(epi == EPI_STAGE ? "DGM_STAGE_CFG" : "DGM_TRACE_CFG");
+  if (!(v && *v)) v = std::getenv("DGM_DENSE_CFG");
   return v && *v ? std::atoi(v) : 0;
 }
 
 template <int EPI, int NHV>
 dgm_status gemm_go_nh(dgm_ctx *c, const GemmArgs &g, cudaStream_t st) {
-  switch (dense_cfg()) {
+  switch (dense_cfg(EPI)) {
     case 1: return gemm_go_c<EPI, Cfg<64, 4, NHV>>(c, g, st);
     case 2: return gemm_go_c<EPI, Cfg<128, 3, NHV>>(c, g, st);
     case 3: return gemm_go_c<EPI, Cfg<32, 4, NHV>>(c, g, st);
