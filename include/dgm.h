@@ -254,10 +254,13 @@ dgm_status dgm_match_faces_host(const dgm_mesh *mesh, int32_t *nbr, int8_t *nbr_
 /* Number of kernel launches the last dgm_step/dgm_apply_* call enqueued. */
 int64_t dgm_last_launches(const dgm_ctx *ctx);
 
-/* Host-only: the reference quadrature of order-`order` contexts with material_points:
- * the collapsed Gauss–Jacobi rule with order+2 points per direction (exact to degree
- * 2·order+3), *Q points ξ_i (xi: [Q][3], may be NULL) and weights (w: [Q], may be
- * NULL).  Point i of element T is X0_T + F_T ξ_i. */
+/* Host-only: the reference quadrature of order-`order` contexts with material_points or
+ * curved elements: the collapsed Gauss–Jacobi rule with order+2 points per direction
+ * (exact to degree 2·order+3), *Q points ξ_i (xi: [Q][3], may be NULL) and weights
+ * (w: [Q], may be NULL).  Point i of element T is X0_T + F_T ξ_i (flat elements) or
+ * Φ_T(ξ_i) (curved elements, the quadratic map of dgm_opts.edge_nodes).  The order of
+ * the points is a outer, c inner in the collapsed coordinates x = (1+a)/2,
+ * y = (1-a)(1+b)/4, z = (1-a)(1-b)(1+c)/8 (the sum-factorised inverse mass relies on it). */
 dgm_status dgm_quadrature_host(int order, int64_t *Q, double *xi, double *w);
 
 /* The engine the context resolved to (DGM_ENGINE_SPARSE, _DENSE or _HYBRID). */
