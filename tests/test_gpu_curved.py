@@ -166,3 +166,19 @@ def test_single_curved_tet(p):
     Er, Hr, _ = symplectic_euler(C, E, H, dt, 20)
     assert _rel(c.to_host(Ed), Er) <= 1e-10
     assert _rel(c.to_host(Hd), Hr) <= 1e-10
+
+
+def test_curved_long_run_graph_replay():
+    """A 70-step dgm_step call (>= 64 steps: the library captures 32 steps into a CUDA
+    graph and replays it) on curved elements with point materials and the hybrid
+    engine (p = 7), against the oracle's time loop."""
+    m, rep, c, C = _case(7, (True,) * 3, 3, seed=11, materials="points")
+    rng = np.random.default_rng(21)
+    E = rng.standard_normal((3, m.n_tet, c.N)) / (1 + np.arange(c.N))
+    H = rng.standard_normal((3, m.n_tet, c.N)) / (1 + np.arange(c.N))
+    dt = 2e-4
+    Ed, Hd = c.to_device(E), c.to_device(H)
+    c.dgm_step(Ed, Hd, dt, 70)
+    Er, Hr, _ = symplectic_euler(C, E, H, dt, 70)
+    assert _rel(c.to_host(Ed), Er) <= 1e-10
+    assert _rel(c.to_host(Hd), Hr) <= 1e-10
