@@ -277,7 +277,7 @@ def run_ours(args, rank, world):
     f64, f64_src = fp64_peak()
     engine = ctx.engine
     kerns = stage_kernels(engine, p)
-    traffic, tsrc = None, None
+    traffic, tsrc, stage_profile = None, None, None
     import glob
     for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
         with open(tpath) as f:
@@ -285,7 +285,13 @@ def run_ours(args, rank, world):
         tr = tj.get(f"{args.config}_{engine}")
         if tr and tr.get("kernels") == kerns:
             traffic = tr["dram_bytes_per_stage"]
-            tsrc = f"{os.path.relpath(tpath, ROOT)} (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum, summed over the stage's kernels)"
+            tsrc = (f"{os.path.relpath(tpath, ROOT)} (ncu --metrics dram__bytes_read.sum + dram__bytes_write.sum, "
+                    f"summed over the stage's kernels, cold cache per replay)")
+            # the stage's kernels from the same capture: cold time, DRAM bytes, pipe use
+            stage_profile = [{"kernel": k.get("kernel"), "ms_cold": k.get("ms"),
+                              "dram_bytes": (k.get("dram_read") or 0) + (k.get("dram_write") or 0),
+                              "dmma_pct": k.get("dmma_pct"), "fp64_pct": k.get("fp64_pct")}
+                             for k in tr.get("per_kernel", [])]
             break
     ach_b = B / per_launch_s / 1e9
     ach_f = Fl / per_launch_s / 1e12
@@ -295,7 +301,7 @@ def run_ours(args, rank, world):
     res["roofline"] = {"bound": bound,
                        "achieved": ach_b if bound == "hbm" else ach_f, "peak": hbm if bound == "hbm" else f64,
                        "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": max(hfrac, ffrac),
-                       "traffic": traffic, "traffic_source": tsrc,
+                       "traffic": traffic, "traffic_source": tsrc, "stage_profile": stage_profile,
                        "hbm": {"achieved": ach_b, "peak": hbm, "unit": "GB/s", "frac": hfrac,
                                "bytes_per_stage": B,
                                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in pk
