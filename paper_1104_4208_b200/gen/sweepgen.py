@@ -37,6 +37,8 @@ from . import relations as R
 
 CH = 16   # modes per chunk (one 128-byte line of an element's coefficient row)
 SPLIT = 4  # recurrences with at least this many terms accumulate in two partial sums
+           # (swept at p = 10, C5 mesh: 2 -> 7.16-7.35, 3 -> 7.26-7.33, 4 -> 6.81-6.98,
+           # 6 -> 7.25-7.30, never -> 7.52-7.64 ms per launch; tools/curlbench/run_split.sh)
 
 
 def n_modes(p):
